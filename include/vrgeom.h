@@ -1,0 +1,196 @@
+/*
+ * vrgeom.h -- C ABI of the B200-native geometry stage (libvrgeom.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `vrlab`
+ * (paths below are relative to /root/reference/pkg/src/vrlab/):
+ *
+ *   index buffer + vertex buffer -> batch formation -> per-batch dedup
+ *   (naive / warp voting / sort / hash) -> vertex shader once per unique
+ *   vertex per batch -> primitive assembly with local-index remap ->
+ *   reuse statistics.
+ *
+ * Conventions
+ *   - every pointer named d_* is DEVICE memory owned by the caller; the library
+ *     never frees caller memory and keeps no state between calls;
+ *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*);
+ *     results are valid after the caller synchronises that stream;
+ *   - calls are re-entrant across streams as long as outputs/workspaces differ;
+ *   - functions return a vr_status; host-detectable misuse is reported
+ *     immediately, data-dependent violations (found by the kernels) are reported
+ *     through vr_stats.error_code / error_batch, read back by the caller;
+ *   - no function falls back to the CPU.  Without a CUDA device every compute
+ *     entry point returns VR_ERR_CUDA.
+ */
+#ifndef VRGEOM_H
+#define VRGEOM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRGEOM_ABI_VERSION 1
+
+/* strategies.py:387  STRATEGY_NAMES = ("naive", "warp", "sort", "hash", "phash") */
+enum vr_strategy {
+    VR_NAIVE = 0, /* strategies.py:159-170 naive_batch          */
+    VR_WARP = 1,  /* strategies.py:173-232 warp_vote_batch      */
+    VR_SORT = 2,  /* strategies.py:235-260 sort_batch           */
+    VR_HASH = 3,  /* strategies.py:263-298 hash_batch           */
+    VR_PHASH = 4  /* strategies.py:301-367 parallel_hash_batch  */
+};
+
+/* OR into the `strategy` argument of vr_run to call a per-batch kernel on its own
+ * (strategies.py:235-298 have no unique budget; the guards of strategies.py:432-435 and
+ * :451-455 belong to run_on_indices). */
+#define VR_FLAG_NO_BUDGET 0x100
+
+enum vr_status {
+    VR_OK = 0,
+    VR_ERR_UNKNOWN_STRATEGY = 1,   /* strategies.py:422-423 ConfigError                    */
+    VR_ERR_BAD_BATCH = 2,          /* strategies.py:426-428 ConfigError (range/alignment)  */
+    VR_ERR_TABLE_BELOW_BUDGET = 3, /* strategies.py:432-435 ConfigError                    */
+    VR_ERR_OVER_BUDGET = 4,        /* strategies.py:451-455 ConfigError (> max_unique)     */
+    VR_ERR_HASH_FULL = 5,          /* strategies.py:283-284, :348-349 RuntimeError         */
+    VR_ERR_WARP_NO_PROGRESS = 6,   /* strategies.py:226-227 RuntimeError                   */
+    VR_ERR_WARP_WIDTH = 7,         /* strategies.py:187-188 ConfigError (w < prim size)    */
+    VR_ERR_UNALIGNED = 8,          /* batching.py:79-80, :96-97 ConfigError                */
+    VR_ERR_BAD_CONFIG = 9,         /* batching.py:44-56, strategies.py:78-86, warp.py:32-35 */
+    VR_ERR_UNSUPPORTED = 10,       /* legal in the reference, outside the device limits    */
+    VR_ERR_CUDA = 11,              /* CUDA runtime failure / no device                     */
+    VR_ERR_CAPACITY = 12,          /* an output buffer is smaller than the result          */
+    VR_ERR_WORKSPACE = 13,         /* workspace smaller than vr_*_workspace_bytes()        */
+    VR_ERR_PRIM_OVER_BUDGET = 14   /* batching.py:119-123 ConfigError                      */
+};
+
+/* batching.py:23-61 BatchConfig (same fields, same defaults: 96/256/1023/32/256/3) */
+typedef struct vr_batch_config {
+    int32_t batch_size;
+    int32_t max_unique;
+    int32_t max_indices;
+    int32_t warp_width;
+    int32_t block_size;
+    int32_t primitive_size;
+} vr_batch_config;
+
+/* strategies.py:70-91 HashConfig (defaults 256 / 2654435769 / 8) */
+typedef struct vr_hash_config {
+    uint32_t table_size;
+    uint32_t multiplier;
+    uint32_t max_fast_probes;
+} vr_hash_config;
+
+/* strategies.py:36-67 ShaderFn: the device shaders are a closed set. */
+enum vr_shader_kind {
+    VR_SHADER_NONE = 0,     /* dedup + assembly only                                        */
+    VR_SHADER_IDENTITY = 1, /* strategies.py:48-50: record = vertex id (== unique_ids)      */
+    VR_SHADER_POSITION = 2  /* strategies.py:53-67: [m @ (x,y,z,1)] / w, FP32               */
+};
+
+typedef struct vr_shader {
+    int32_t kind;              /* vr_shader_kind                                             */
+    int32_t has_matrix;        /* 0: record = position as is (strategies.py:56-58)           */
+    float matrix[16];          /* row-major 4x4 (strategies.py:60-65)                        */
+    const float *d_positions4; /* float4[vertex_count] = (x, y, z, 1); 16-byte aligned       */
+    const uint32_t *d_attributes; /* optional opaque per-vertex payload (mesh.py:40-41), or NULL */
+    int32_t attr_words;        /* 32-bit words of payload per vertex                         */
+    int32_t vertex_count;      /* 0 if unknown; needed for d_shade_counts                    */
+} vr_shader;
+
+/* Statistics block: int64[VR_STATS_WORDS] in device memory, written by vr_run.
+ * analytics.py:20-50 ReuseReport + strategies.py:94-111 ProbeStats. */
+enum vr_stats_word {
+    VR_STAT_INDICES = 0,     /* indices consumed                         */
+    VR_STAT_INVOCATIONS = 1, /* shader invocations                       */
+    VR_STAT_BATCHES = 2,
+    VR_STAT_ROUNDS = 3,
+    VR_STAT_PROBES_FAST = 4,
+    VR_STAT_PROBES_SLOW = 5,
+    VR_STAT_PROBE_MAX_CHAIN = 6,
+    VR_STAT_ERROR = 7, /* (first failing batch << 8) | vr_status, or -1 when clean */
+    VR_STATS_WORDS = 16
+};
+
+/* Flattened list of DedupResult (strategies.py:114-129), batch order.
+ * Any pointer except d_stats may be NULL when that output is not wanted
+ * (d_shaded is required for VR_SHADER_POSITION). */
+typedef struct vr_outputs {
+    int32_t *d_batch_round_off; /* [n_batches+1] first round of each batch                  */
+    int32_t *d_round_uid_off;   /* [rounds+1]    first unique id of each round              */
+    int32_t *d_round_prims;     /* [rounds]      Round.primitives_emitted                   */
+    uint32_t *d_unique_ids;     /* [invocations] Round.unique_ids, concatenated             */
+    uint16_t *d_assembly_map;   /* [sum of batch spans] Round.assembly_map, concatenated    */
+    float *d_shaded4;           /* float4[invocations] = (x/w, y/w, z/w, w)                 */
+    uint32_t *d_shaded_attr;    /* [invocations * attr_words] pass-through payload          */
+    int32_t *d_shade_counts;    /* [vertex_count] per-vertex tally (strategies.py:485-489);
+                                   must be zeroed by the caller                              */
+    int64_t *d_stats;           /* [VR_STATS_WORDS]                                          */
+    int64_t cap_unique;         /* capacity of d_unique_ids / d_shaded4 (elements)           */
+    int64_t cap_rounds;         /* capacity of d_round_prims (elements)                      */
+} vr_outputs;
+
+int vr_abi_version(void);
+const char *vr_status_string(int status);
+
+/* Number of CUDA devices visible, or 0 (never fails). */
+int vr_device_count(void);
+
+/* Validation of the two parameter blocks (batching.py:44-56; strategies.py:78-86). */
+int vr_check_batch_config(const vr_batch_config *cfg);
+int vr_check_hash_config(const vr_hash_config *hcfg);
+
+/* batching.py:76-84 static_batches.  Writes ceil(n/batch_size)+1 offsets
+ * (the "auxiliary buffer" of batching.py:128-137) to d_offsets. */
+int64_t vr_static_batch_count(int64_t n_indices, const vr_batch_config *cfg);
+int vr_static_offsets(int64_t n_indices, const vr_batch_config *cfg, int32_t *d_offsets, void *stream);
+
+/* batching.py:87-125 dynamic_batches: exact parallel restatement of the greedy scan.
+ * d_offsets must hold n_indices/primitive_size + 1 entries; d_n_batches is device int64[2]:
+ * [0] receives the batch count (0 for an empty buffer), [1] a vr_status found on the device. */
+size_t vr_dynamic_workspace_bytes(int64_t n_indices, const vr_batch_config *cfg);
+int vr_dynamic_batches(const uint32_t *d_indices, int64_t n_indices, const vr_batch_config *cfg,
+                       int32_t *d_offsets, int64_t *d_n_batches, void *d_workspace,
+                       size_t workspace_bytes, void *stream);
+
+/* Upper bounds for the data-dependent output sizes of vr_run. */
+int vr_output_bounds(int strategy, int64_t span_total, int64_t n_batches, const vr_batch_config *cfg,
+                     const vr_hash_config *hcfg, int64_t *max_invocations, int64_t *max_rounds);
+
+size_t vr_run_workspace_bytes(int strategy, int64_t span_total, int64_t n_batches,
+                              const vr_batch_config *cfg, const vr_hash_config *hcfg);
+
+/* strategies.py:404-502 run_on_indices on device.
+ * d_batch_begin / d_batch_end: int32[n_batches] half-open ranges (batching.py:64-73); for a
+ * contiguous offsets array pass (offsets, offsets + 1).  span_total >= the sum of the batch
+ * spans (n_indices when the batches tile the buffer; it sizes d_assembly_map and the
+ * workspace), max_span >= the longest batch. */
+int vr_run(int strategy, const uint32_t *d_indices, int64_t n_indices, const int32_t *d_batch_begin,
+           const int32_t *d_batch_end, int64_t n_batches, int64_t span_total, int32_t max_span,
+           const vr_batch_config *cfg, const vr_hash_config *hcfg, const vr_shader *shader,
+           const vr_outputs *out, void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* strategies.py:456-463 + :132-152: expanded per-corner record stream,
+ * out[slot] = shaded[round base + assembly_map[slot]].  d_stream_pos3 is float[3*n_slots]
+ * (TriangleStream.as_array() for the position shader), d_stream_ids uint32[n_slots]
+ * (identity shader); either may be NULL. */
+int vr_expand_stream(const int32_t *d_batch_round_off, const int32_t *d_round_uid_off,
+                     const int32_t *d_round_prims, const uint16_t *d_assembly_map,
+                     const uint32_t *d_unique_ids, const float *d_shaded4, int64_t n_batches,
+                     const int32_t *d_batch_begin, const int32_t *d_batch_end, int32_t primitive_size,
+                     float *d_stream_pos3, uint32_t *d_stream_ids, void *d_workspace,
+                     size_t workspace_bytes, void *stream);
+
+/* Profiling aid (bench.py): per-kernel device time of the last vr_run, measured with CUDA
+ * events on the launching stream.  Stages, in order: span scan, dedup, count scan,
+ * shade/finalize, statistics.  Process-wide; do not enable under concurrent vr_run calls.
+ * vr_profile_read synchronises the last event and returns the number of stages written. */
+#define VR_PROFILE_STAGES 5
+int vr_profile_enable(int on);
+int vr_profile_read(float *ms, int cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VRGEOM_H */

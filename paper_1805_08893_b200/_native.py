@@ -1,0 +1,117 @@
+"""ctypes binding of libvrgeom.so (include/vrgeom.h).  There is no CPU fallback: every
+compute entry point raises if the CUDA extension or a CUDA device is missing."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvrgeom.so")
+
+VR_NAIVE, VR_WARP, VR_SORT, VR_HASH, VR_PHASH = range(5)
+STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_HASH, "phash": VR_PHASH}
+
+(VR_OK, VR_ERR_UNKNOWN_STRATEGY, VR_ERR_BAD_BATCH, VR_ERR_TABLE_BELOW_BUDGET, VR_ERR_OVER_BUDGET,
+ VR_ERR_HASH_FULL, VR_ERR_WARP_NO_PROGRESS, VR_ERR_WARP_WIDTH, VR_ERR_UNALIGNED, VR_ERR_BAD_CONFIG,
+ VR_ERR_UNSUPPORTED, VR_ERR_CUDA, VR_ERR_CAPACITY, VR_ERR_WORKSPACE, VR_ERR_PRIM_OVER_BUDGET) = range(15)
+
+VR_FLAG_NO_BUDGET = 0x100
+
+VR_SHADER_NONE, VR_SHADER_IDENTITY, VR_SHADER_POSITION = range(3)
+
+(VR_STAT_INDICES, VR_STAT_INVOCATIONS, VR_STAT_BATCHES, VR_STAT_ROUNDS, VR_STAT_PROBES_FAST,
+ VR_STAT_PROBES_SLOW, VR_STAT_PROBE_MAX_CHAIN, VR_STAT_ERROR) = range(8)
+VR_STATS_WORDS = 16
+VR_PROFILE_STAGES = 5
+PROFILE_STAGE_NAMES = ("span_scan", "dedup", "count_scan", "shade_finalize", "stats")
+
+
+class NativeLibraryError(RuntimeError):
+    """libvrgeom.so is missing or no CUDA device is visible."""
+
+
+class BatchConfigC(C.Structure):
+    _fields_ = [("batch_size", C.c_int32), ("max_unique", C.c_int32), ("max_indices", C.c_int32),
+                ("warp_width", C.c_int32), ("block_size", C.c_int32), ("primitive_size", C.c_int32)]
+
+
+class HashConfigC(C.Structure):
+    _fields_ = [("table_size", C.c_uint32), ("multiplier", C.c_uint32), ("max_fast_probes", C.c_uint32)]
+
+
+class ShaderC(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("has_matrix", C.c_int32), ("matrix", C.c_float * 16),
+                ("d_positions4", C.c_void_p), ("d_attributes", C.c_void_p), ("attr_words", C.c_int32),
+                ("vertex_count", C.c_int32)]
+
+
+class OutputsC(C.Structure):
+    _fields_ = [("d_batch_round_off", C.c_void_p), ("d_round_uid_off", C.c_void_p),
+                ("d_round_prims", C.c_void_p), ("d_unique_ids", C.c_void_p),
+                ("d_assembly_map", C.c_void_p), ("d_shaded4", C.c_void_p),
+                ("d_shaded_attr", C.c_void_p), ("d_shade_counts", C.c_void_p), ("d_stats", C.c_void_p),
+                ("cap_unique", C.c_int64), ("cap_rounds", C.c_int64)]
+
+
+_lib = None
+
+_SIGNATURES = {
+    "vr_abi_version": (C.c_int, []),
+    "vr_status_string": (C.c_char_p, [C.c_int]),
+    "vr_device_count": (C.c_int, []),
+    "vr_check_batch_config": (C.c_int, [C.POINTER(BatchConfigC)]),
+    "vr_check_hash_config": (C.c_int, [C.POINTER(HashConfigC)]),
+    "vr_static_batch_count": (C.c_int64, [C.c_int64, C.POINTER(BatchConfigC)]),
+    "vr_static_offsets": (C.c_int, [C.c_int64, C.POINTER(BatchConfigC), C.c_void_p, C.c_void_p]),
+    "vr_dynamic_workspace_bytes": (C.c_size_t, [C.c_int64, C.POINTER(BatchConfigC)]),
+    "vr_dynamic_batches": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(BatchConfigC), C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_output_bounds": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.POINTER(BatchConfigC),
+                                   C.POINTER(HashConfigC), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "vr_run_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int64, C.c_int64, C.POINTER(BatchConfigC),
+                                            C.POINTER(HashConfigC)]),
+    "vr_run": (C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                         C.c_int32, C.POINTER(BatchConfigC), C.POINTER(HashConfigC), C.POINTER(ShaderC),
+                         C.POINTER(OutputsC), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_profile_enable": (C.c_int, [C.c_int]),
+    "vr_profile_read": (C.c_int, [C.POINTER(C.c_float), C.c_int]),
+    "vr_expand_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_size_t, C.c_void_p]),
+}
+
+
+def exported_symbols():
+    """Every entry point include/vrgeom.h declares."""
+    return tuple(_SIGNATURES)
+
+
+def lib():
+    """Load libvrgeom.so (built in-tree by __graft_entry__.build()).  Raises loudly if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise NativeLibraryError(
+                f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`; "
+                "this package has no CPU fallback")
+        handle = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        if handle.vr_abi_version() != 1:
+            raise NativeLibraryError("libvrgeom.so ABI version mismatch")
+        _lib = handle
+    return _lib
+
+
+def require_cuda():
+    """The hot path runs on a B200 or not at all."""
+    handle = lib()
+    if handle.vr_device_count() < 1:
+        raise NativeLibraryError("no CUDA device visible: the geometry stage has no CPU fallback")
+    return handle
+
+
+def status_string(status: int) -> str:
+    return lib().vr_status_string(status).decode()

@@ -1,0 +1,105 @@
+// vr_common.cuh -- shared device helpers for libvrgeom (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/vrgeom.h"
+
+namespace vr {
+
+constexpr int kWarp = 32;
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // mesh.py:11-13: reserved, never a vertex id
+
+#define VR_CUDA_CHECK(expr)                         \
+    do {                                            \
+        cudaError_t _e = (expr);                    \
+        if (_e != cudaSuccess) return VR_ERR_CUDA;  \
+    } while (0)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline uint32_t next_pow2(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+__host__ __device__ inline int ilog2(uint32_t pow2) {
+    int b = 0;
+    while ((1u << b) < pow2) b++;
+    return b;
+}
+
+// First failing batch wins, as in the reference's in-order loop (strategies.py:470):
+// word = (batch << 8) | status, reduced with a signed 64-bit min; -1 == clean is
+// stored as INT64_MAX internally and rewritten by the finalize kernel.
+__device__ inline void report_error(int64_t* stats, int64_t batch, int status) {
+    long long word = (long long)((batch << 8) | (int64_t)status);
+    atomicMin((long long*)&stats[VR_STAT_ERROR], word);
+}
+
+// strategies.py:88-91 HashConfig.slot; bits == 0 (table_size 1) -> slot 0.
+__device__ __forceinline__ uint32_t hash_slot(uint32_t vid, uint32_t mult, int bits) {
+    uint32_t prod = vid * mult;
+    return bits == 0 ? 0u : (prod >> (32 - bits));
+}
+
+__device__ __forceinline__ int warp_incl_scan(int v, int lane) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+// Exclusive scan of data[0..n) in shared memory by the whole CTA (any blockDim that is a
+// multiple of 32, <= 1024).  Returns the total.  `scratch` holds >= 33 ints.
+__device__ inline int block_exclusive_scan(int* data, int n, int* scratch) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (n + nt - 1) / nt;
+    const int lo = min(n, tid * per), hi = min(n, lo + per);
+    int sum = 0;
+    for (int i = lo; i < hi; i++) sum += data[i];
+    int inc = warp_incl_scan(sum, lane);
+    if (lane == 31) scratch[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        int nw = nt >> 5;
+        int w = lane < nw ? scratch[lane] : 0;
+        int winc = warp_incl_scan(w, lane);
+        scratch[lane] = winc - w;  // exclusive warp offsets
+        if (lane == 31) scratch[32] = winc;
+    }
+    __syncthreads();
+    int run = scratch[wid] + inc - sum;
+    const int total = scratch[32];
+    for (int i = lo; i < hi; i++) {
+        int v = data[i];
+        data[i] = run;
+        run += v;
+    }
+    __syncthreads();
+    return total;
+}
+
+// strategies.py:53-67 position_shader in FP32: record = (m @ [x,y,z,1])[:3] / w.
+struct ShaderParams {
+    int kind;
+    int has_matrix;
+    float m[16];
+    const float4* __restrict__ pos4;
+    const uint32_t* __restrict__ attr;
+    int attr_words;
+    int vertex_count;
+};
+
+__device__ __forceinline__ float4 shade_position(const ShaderParams& sp, uint32_t vid) {
+    float4 p = __ldg(sp.pos4 + vid);
+    if (!sp.has_matrix) return make_float4(p.x, p.y, p.z, 1.0f);
+    float ox = fmaf(sp.m[0], p.x, fmaf(sp.m[1], p.y, fmaf(sp.m[2], p.z, sp.m[3])));
+    float oy = fmaf(sp.m[4], p.x, fmaf(sp.m[5], p.y, fmaf(sp.m[6], p.z, sp.m[7])));
+    float oz = fmaf(sp.m[8], p.x, fmaf(sp.m[9], p.y, fmaf(sp.m[10], p.z, sp.m[11])));
+    float ow = fmaf(sp.m[12], p.x, fmaf(sp.m[13], p.y, fmaf(sp.m[14], p.z, sp.m[15])));
+    return make_float4(__fdiv_rn(ox, ow), __fdiv_rn(oy, ow), __fdiv_rn(oz, ow), ow);
+}
+
+}  // namespace vr

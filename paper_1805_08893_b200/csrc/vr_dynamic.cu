@@ -1,0 +1,315 @@
+// vr_dynamic.cu -- exact parallel restatement of the greedy dynamic batch splitter
+// (/root/reference/pkg/src/vrlab/batching.py:87-125).
+//
+// The reference walks the index buffer front to back with a Python set: a primitive joins the
+// open batch iff |uniques U prim| <= max_unique and the primitive cap is not exceeded, except
+// that the first primitive of a batch is always accepted (batching.py:106-118).  Every batch
+// boundary depends on the previous one, so the scan is restated as two exact stages:
+//
+//  Stage A  next[s] = end of the greedy batch that would START at primitive s.  It depends on
+//           s alone:  next[s] = max e <= min(T, s+cap) with
+//                     #{ i in [ps*s, ps*e) : prev_occurrence(i) < ps*s } <= max_unique, e > s.
+//           A1 (occurrence_links): nearest earlier / later position holding the same id,
+//              exact within one batch window, from a per-warp shared-memory table walked in
+//              32-wide steps (__match_any_sync orders duplicates inside a step).
+//           A2 (greedy_next): every thread slides a two-pointer window over its own run of
+//              start primitives; appending index i adds a unique iff prev[i] < window start,
+//              retiring index i removes one iff nxt[i] >= window end.  No set, no hashing.
+//  Stage B  the boundaries are the chain b0 = 0, b(k+1) = next[b(k)].  A chunk of the stream
+//           is a function "entry offset -> (exit offset, batches emitted)"; these functions
+//           compose associatively, so the chain is resolved by a reduce-then-scan over chunk
+//           tables (B1 chunk tables, B2 group tables, B3 group scan, B4 chunk entries) and
+//           B5 writes the offsets array (batching.py:128-137).
+#include "vr_common.cuh"
+
+namespace vr {
+
+constexpr int kNoLink = 0x7fffffff;  // "no later occurrence"
+constexpr int kGroup = 64;           // chunks per group in the two-level scan
+
+struct DynCtx {
+    const uint32_t* __restrict__ ids;
+    int n;        // indices
+    int T;        // primitives
+    int ps;
+    int max_unique;
+    int cap;      // max primitives per batch (batching.py:58-61)
+    int window;   // ps * cap positions
+    int tile;     // positions per A1 tile (multiple of 32)
+    int slots;    // A1 table slots (power of two)
+    int chunk;    // primitives per chunk, >= cap
+    int n_chunks;
+    int n_groups;
+    int32_t* prev;
+    int32_t* nxt;
+    int32_t* next;     // [T]
+    int32_t* c_exit;   // [n_chunks * cap]
+    int32_t* c_cnt;    // [n_chunks * cap]
+    int32_t* g_exit;   // [n_groups * cap]
+    int32_t* g_cnt;    // [n_groups * cap]
+    int32_t* g_entry;  // [n_groups + 1]
+    int32_t* g_base;   // [n_groups + 1]
+    int32_t* c_entry;  // [n_chunks]
+    int32_t* c_base;   // [n_chunks]
+    int32_t* offsets;  // out
+    int64_t* n_batches;  // out: [0] count, [1] status
+};
+
+__global__ void fill_kernel(int32_t* p, int n, int v) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+// ---- A1 -----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_tiles) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int tile_id = blockIdx.x * (blockDim.x >> 5) + wid;
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wid * 2 * c.slots;
+    int32_t* last = reinterpret_cast<int32_t*>(keys + c.slots);
+    if (tile_id >= n_tiles) return;
+    const uint32_t mask = (uint32_t)c.slots - 1;
+    const int sbits = ilog2((uint32_t)c.slots);
+    for (int i = lane; i < c.slots; i += 32) keys[i] = kEmpty;
+    __syncwarp();
+    const int t0 = tile_id * c.tile;
+    const int t1 = min(c.n, t0 + c.tile);
+    int hs = t0 - c.window;
+    hs = hs < 0 ? 0 : (hs & ~31);
+    const uint32_t lt = (1u << lane) - 1;
+    for (int base = hs; base < t1; base += 32) {
+        const int i = base + lane;
+        const bool valid = i < t1;
+        const uint32_t id = valid ? c.ids[i] : kEmpty;
+        const uint32_t peers = __match_any_sync(0xffffffffu, id);
+        const uint32_t lower = peers & lt;
+        const bool leader = valid && lower == 0;
+        const int hipeer = 31 - __clz(peers);
+        uint32_t h = (id * 0x9E3779B1u) >> (32 - sbits);
+        bool active = leader, existed = false;
+        while (__any_sync(0xffffffffu, active)) {
+            uint32_t k = active ? keys[h] : 0u;
+            bool claim = active && k == kEmpty;
+            if (active && k == id) { existed = true; active = false; }
+            if (claim) keys[h] = id;
+            __syncwarp();
+            if (claim) {
+                if (keys[h] == id) active = false; else h = (h + 1) & mask;
+            } else if (active) {
+                h = (h + 1) & mask;
+            }
+            __syncwarp();
+        }
+        int pv = -1;
+        if (leader) {
+            if (existed) pv = last[h];
+            last[h] = base + hipeer;
+        } else if (valid) {
+            pv = base + (31 - __clz(lower));
+        }
+        __syncwarp();
+        if (valid && i >= t0) {
+            c.prev[i] = pv;
+            if (pv >= 0) c.nxt[pv] = i;
+        }
+    }
+}
+
+// ---- A2 -----------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) greedy_next_kernel(DynCtx c, int run) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int s0 = t * run;
+    if (s0 >= c.T) return;
+    const int s1 = min(c.T, s0 + run);
+    const int ps = c.ps;
+    int e = s0, cnt = 0;
+    for (int s = s0; s < s1; s++) {
+        const int S = ps * s;
+        const int lim = min(c.T, s + c.cap);
+        if (e < s) { e = s; cnt = 0; }
+        while (e < lim) {
+            int fresh = 0;
+            for (int k = 0; k < ps; k++) fresh += c.prev[ps * e + k] < S;
+            if (e != s && cnt + fresh > c.max_unique) break;  // first primitive always accepted
+            cnt += fresh;
+            e++;
+        }
+        c.next[s] = e;
+        const int E = ps * e;
+        int lost = 0;
+        for (int k = 0; k < ps; k++) lost += c.nxt[S + k] >= E;
+        cnt -= lost;
+    }
+}
+
+// ---- B1: chunk tables ---------------------------------------------------------------------
+__global__ void __launch_bounds__(256) chunk_table_kernel(DynCtx c) {
+    const int k = blockIdx.x;
+    const int lo = k * c.chunk, hi = min(c.T, lo + c.chunk);
+    for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
+        int s = lo + o, cnt = 0;
+        while (s < hi) { s = c.next[s]; cnt++; }
+        // entries at or past the end of the stream emit nothing and exit at offset 0
+        c.c_exit[(size_t)k * c.cap + o] = s >= hi ? s - hi : 0;
+        c.c_cnt[(size_t)k * c.cap + o] = cnt;
+    }
+}
+
+// ---- B2: group tables (compose kGroup chunk tables for every entry offset) -----------------
+__global__ void __launch_bounds__(256) group_table_kernel(DynCtx c) {
+    const int g = blockIdx.x;
+    const int k0 = g * kGroup, k1 = min(c.n_chunks, k0 + kGroup);
+    for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
+        int e = o, cnt = 0;
+        for (int k = k0; k < k1; k++) {
+            size_t at = (size_t)k * c.cap + e;
+            cnt += c.c_cnt[at];
+            e = c.c_exit[at];
+        }
+        c.g_exit[(size_t)g * c.cap + o] = e;
+        c.g_cnt[(size_t)g * c.cap + o] = cnt;
+    }
+}
+
+// ---- B3: scan over groups (one thread; n_groups is T / (chunk * kGroup)) --------------------
+__global__ void group_scan_kernel(DynCtx c) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int e = 0, base = 0;
+    for (int g = 0; g < c.n_groups; g++) {
+        c.g_entry[g] = e;
+        c.g_base[g] = base;
+        size_t at = (size_t)g * c.cap + e;
+        base += c.g_cnt[at];
+        e = c.g_exit[at];
+    }
+    c.g_entry[c.n_groups] = e;
+    c.g_base[c.n_groups] = base;
+    c.n_batches[0] = base;
+    c.n_batches[1] = 0;
+    c.offsets[base] = c.n;  // batching.py:124,136: last entry = end of the final batch
+}
+
+// ---- B4: true entry offset / first batch number of every chunk -----------------------------
+__global__ void __launch_bounds__(128) chunk_entry_kernel(DynCtx c) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= c.n_groups) return;
+    const int k0 = g * kGroup, k1 = min(c.n_chunks, k0 + kGroup);
+    int e = c.g_entry[g], base = c.g_base[g];
+    for (int k = k0; k < k1; k++) {
+        c.c_entry[k] = e;
+        c.c_base[k] = base;
+        size_t at = (size_t)k * c.cap + e;
+        base += c.c_cnt[at];
+        e = c.c_exit[at];
+    }
+}
+
+// ---- B5: offsets ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) emit_offsets_kernel(DynCtx c) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= c.n_chunks) return;
+    const int lo = k * c.chunk, hi = min(c.T, lo + c.chunk);
+    int s = lo + c.c_entry[k], j = c.c_base[k];
+    while (s < hi) {
+        c.offsets[j++] = s * c.ps;
+        s = c.next[s];
+    }
+}
+
+static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct DynLayout {
+    size_t prev, nxt, next, c_exit, c_cnt, g_exit, g_cnt, g_entry, g_base, c_entry, c_base, total;
+    int T, cap, chunk, n_chunks, n_groups, tile, slots, window;
+};
+
+static DynLayout dyn_layout(int64_t n, const vr_batch_config* cfg) {
+    DynLayout L{};
+    const int ps = cfg->primitive_size;
+    L.T = (int)(n / ps);
+    int64_t cap = cfg->max_indices / ps;
+    if (cap > L.T) cap = L.T > 0 ? L.T : 1;
+    L.cap = (int)cap;
+    L.window = L.cap * ps;
+    L.chunk = L.cap > 1024 ? L.cap : 1024;
+    L.n_chunks = (int)ceil_div(L.T > 0 ? L.T : 1, L.chunk);
+    L.n_groups = (int)ceil_div(L.n_chunks, kGroup);
+    int tile = (L.window + 31) & ~31;
+    if (tile < 1024) tile = 1024;
+    L.tile = tile;
+    L.slots = (int)next_pow2((uint32_t)(2 * (tile + ((L.window + 31) & ~31) + 32)));
+    size_t o = 0;
+    L.prev = o; o += al((size_t)n * 4 + 64);
+    L.nxt = o; o += al((size_t)n * 4 + 64);
+    L.next = o; o += al((size_t)L.T * 4 + 64);
+    L.c_exit = o; o += al((size_t)L.n_chunks * L.cap * 4);
+    L.c_cnt = o; o += al((size_t)L.n_chunks * L.cap * 4);
+    L.g_exit = o; o += al((size_t)L.n_groups * L.cap * 4);
+    L.g_cnt = o; o += al((size_t)L.n_groups * L.cap * 4);
+    L.g_entry = o; o += al((size_t)(L.n_groups + 1) * 4);
+    L.g_base = o; o += al((size_t)(L.n_groups + 1) * 4);
+    L.c_entry = o; o += al((size_t)L.n_chunks * 4);
+    L.c_base = o; o += al((size_t)L.n_chunks * 4);
+    L.total = o;
+    return L;
+}
+
+}  // namespace vr
+
+using namespace vr;
+
+extern "C" {
+
+size_t vr_dynamic_workspace_bytes(int64_t n, const vr_batch_config* cfg) {
+    if (vr_check_batch_config(cfg) || n <= 0 || n > 0x7fffffffLL) return 0;
+    return dyn_layout(n, cfg).total;
+}
+
+int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg, int32_t* d_offsets,
+                       int64_t* d_n_batches, void* d_ws, size_t ws_bytes, void* stream_) {
+    int st = vr_check_batch_config(cfg);
+    if (st) return st;
+    if (n % cfg->primitive_size != 0) return VR_ERR_UNALIGNED;  // batching.py:96-97
+    if (n < 0 || n > 0x7fffffffLL) return VR_ERR_UNSUPPORTED;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (n == 0) {  // batching.py:99-100
+        VR_CUDA_CHECK(cudaMemsetAsync(d_n_batches, 0, 16, stream));
+        return VR_OK;
+    }
+    DynLayout L = dyn_layout(n, cfg);
+    if (!d_ws || ws_bytes < L.total) return VR_ERR_WORKSPACE;
+    const int warps_per_cta = 4;
+    size_t smem = (size_t)warps_per_cta * L.slots * 8;
+    int wpc = warps_per_cta;
+    while (smem > 200 * 1024 && wpc > 1) { wpc >>= 1; smem = (size_t)wpc * L.slots * 8; }
+    if (smem > 200 * 1024) return VR_ERR_UNSUPPORTED;  // batch window too long for the link table
+    unsigned char* ws = (unsigned char*)d_ws;
+    DynCtx c{};
+    c.ids = d_idx; c.n = (int)n; c.T = L.T; c.ps = cfg->primitive_size; c.max_unique = cfg->max_unique;
+    c.cap = L.cap; c.window = L.window; c.tile = L.tile; c.slots = L.slots; c.chunk = L.chunk;
+    c.n_chunks = L.n_chunks; c.n_groups = L.n_groups;
+    c.prev = (int32_t*)(ws + L.prev); c.nxt = (int32_t*)(ws + L.nxt); c.next = (int32_t*)(ws + L.next);
+    c.c_exit = (int32_t*)(ws + L.c_exit); c.c_cnt = (int32_t*)(ws + L.c_cnt);
+    c.g_exit = (int32_t*)(ws + L.g_exit); c.g_cnt = (int32_t*)(ws + L.g_cnt);
+    c.g_entry = (int32_t*)(ws + L.g_entry); c.g_base = (int32_t*)(ws + L.g_base);
+    c.c_entry = (int32_t*)(ws + L.c_entry); c.c_base = (int32_t*)(ws + L.c_base);
+    c.offsets = d_offsets; c.n_batches = d_n_batches;
+
+    fill_kernel<<<(int)ceil_div(n, 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
+    const int n_tiles = (int)ceil_div(n, L.tile);
+    VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    occurrence_links_kernel<<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles);
+    const int run = 64;
+    const int n_threads = (int)ceil_div(L.T, run);
+    greedy_next_kernel<<<(int)ceil_div(n_threads, 128), 128, 0, stream>>>(c, run);
+    chunk_table_kernel<<<L.n_chunks, 256, 0, stream>>>(c);
+    group_table_kernel<<<L.n_groups, 256, 0, stream>>>(c);
+    group_scan_kernel<<<1, 32, 0, stream>>>(c);
+    chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
+    emit_offsets_kernel<<<(int)ceil_div(L.n_chunks, 128), 128, 0, stream>>>(c);
+    VR_CUDA_CHECK(cudaGetLastError());
+    return VR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+"""Full-size configs (BASELINE.json configs[2], configs[3]): the oracle's goldens from
+BASELINE.md plus size-independent properties (stream == input, tally sums, monotone offsets)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1805_08893_b200 as P
+from helpers import assert_flat_equal, oracle_flat
+from paper_1805_08893_b200 import _native as N
+from paper_1805_08893_b200 import engine
+from paper_1805_08893_b200.batching import BatchConfig
+from paper_1805_08893_b200.strategies import HashConfig
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dragon_grid():
+    mesh = P.gen_grid(1898, 1898)
+    assert (mesh.vertex_count, mesh.triangle_count, len(mesh.indices)) == (3602404, 7197218, 21591654)
+    return mesh
+
+
+def test_config3_warp(cuda_lib, dragon_grid):
+    """224 914 batches, 449 827 rounds, 8 100 190 invocations."""
+    mesh = dragon_grid
+    cfg = BatchConfig()
+    d_idx = engine.to_device_indices(mesh.indices)
+    offs = engine.static_offsets_device(len(mesh.indices), cfg)
+    nb = offs.numel() - 1
+    spec = engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY, vertex_count=mesh.vertex_count)
+    run = engine.run_device("warp", d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 96, cfg, None, spec,
+                            want_counts=True).check()
+    assert (nb, run.rounds, run.invocations) == (224914, 449827, 8100190)
+    assert abs(1 - run.invocations / run.indices - 0.624846) < 1e-6
+    assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
+    assert int(run.shade_counts.sum().item()) == run.invocations
+    # bit-exact against the oracle on a prefix and on a window in the middle of the stream
+    for lo in (0, 3000 * 96 * 30):
+        sub = mesh.indices[lo:lo + 96 * 3000]
+        so = O.static_batches(len(sub))
+        fr = O.run("warp", sub, so[:-1], so[1:])
+        import torch
+        o = torch.from_numpy(so.astype(np.int32)).cuda()
+        r = engine.run_device("warp", engine.to_device_indices(sub), o[:-1], o[1:], len(so) - 1, len(sub), 96,
+                              cfg, None, engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
+        assert_flat_equal(r.flat(), oracle_flat(fr), f"window {lo}")
+
+
+def test_config3_mesh_dynamic_sort(cuda_lib, dragon_grid):
+    """dynamic 256/1023 on the strip-ordered mesh: 28 350 batches, 7 257 500 invocations."""
+    mesh = dragon_grid
+    cfg = BatchConfig()
+    d_idx = engine.to_device_indices(mesh.indices)
+    offs = engine.dynamic_offsets_device(d_idx, cfg)
+    nb = offs.numel() - 1
+    assert nb == 28350
+    run = engine.run_device("sort", d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 1023, cfg, None,
+                            engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY)).check()
+    assert run.invocations == 7257500
+    assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
+    h = offs.cpu().numpy().astype(np.int64)
+    assert np.array_equal(h[:4000], O.dynamic_batches(mesh.indices[:int(h[4000])])[:4000])
+
+
+def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
+    """84 672 batches, 21 591 005 invocations, probes 216 377 586 / chain 256."""
+    mesh = P.shuffle_triangles(dragon_grid, 0)
+    assert list(mesh.indices[:6]) == [3502237, 3504135, 3502238, 2050717, 2052615, 2050718]
+    cfg = BatchConfig()
+    d_idx = engine.to_device_indices(mesh.indices)
+    offs = engine.dynamic_offsets_device(d_idx, cfg)
+    nb = offs.numel() - 1
+    assert nb == 84672
+    h = offs.cpu().numpy().astype(np.int64)
+    assert h[0] == 0 and h[-1] == len(mesh.indices) and (np.diff(h) > 0).all() and (np.diff(h) % 3 == 0).all()
+    k = 3000
+    assert np.array_equal(h[:k], O.dynamic_batches(mesh.indices[:int(h[k])])[:k])
+    for strat in ("hash", "sort"):
+        run = engine.run_device(strat, d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 1023, cfg,
+                                HashConfig(), engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY)).check()
+        assert run.invocations == 21591005
+        if strat == "hash":
+            assert run.probes == (216377586, 0, 256)
+        assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
+        sub_offs = h[:k + 1]
+        fr = O.run(strat, mesh.indices, sub_offs[:-1], sub_offs[1:])
+        sub = engine.run_device(strat, d_idx, offs[:k], offs[1:k + 1], k, int(sub_offs[-1]), 1023, cfg,
+                                HashConfig(), engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
+        assert_flat_equal(sub.flat(), oracle_flat(fr), f"config4 {strat} prefix")

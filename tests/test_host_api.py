@@ -1,0 +1,202 @@
+"""CPU-only checks of the host mirror of the reference API and of the C-ABI boundary
+(no compute calls: there is no GPU in the build container)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_1805_08893_b200 as P
+from paper_1805_08893_b200 import _native, build
+from paper_1805_08893_b200.batching import Batch, BatchConfig, ConfigError
+from paper_1805_08893_b200.strategies import HashConfig, ProbeStats, effective_workers
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class TestBatchConfig:  # reference tests/test_batching.py:17-42
+    def test_defaults(self):
+        cfg = BatchConfig()
+        assert (cfg.batch_size, cfg.max_unique, cfg.max_indices, cfg.max_primitives) == (96, 256, 1023, 341)
+        assert (cfg.warp_width, cfg.block_size, cfg.primitive_size) == (32, 256, 3)
+
+    def test_validation(self):
+        for bad in (dict(batch_size=97), dict(batch_size=0), dict(max_unique=2), dict(max_indices=2),
+                    dict(block_size=0), dict(primitive_size=0)):
+            with pytest.raises(ConfigError):
+                BatchConfig(**bad)
+        BatchConfig(max_unique=3)
+        assert BatchConfig(primitive_size=1, max_unique=1).max_primitives == 1023
+        with pytest.raises(ValueError):
+            BatchConfig(warp_width=12)
+
+
+class TestStaticBatches:  # reference tests/test_batching.py:44-68
+    def test_cases(self):
+        cfg = BatchConfig()
+        assert P.static_batches(192, cfg) == [Batch(0, 96), Batch(96, 192)]
+        assert P.static_batches(99, cfg) == [Batch(0, 96), Batch(96, 99)]
+        assert P.static_batches(0, cfg) == []
+        with pytest.raises(ConfigError):
+            P.static_batches(100, cfg)
+        batches = P.static_batches(606, BatchConfig(batch_size=12))
+        assert batches[0].begin == 0 and batches[-1].end == 606
+        assert all(a.end == b.begin for a, b in zip(batches, batches[1:]))
+
+
+def test_offsets_roundtrip():  # reference tests/test_batching.py:123-131
+    batches = [Batch(0, 96), Batch(96, 120), Batch(120, 300)]
+    offs = P.batches_to_offsets(batches)
+    assert list(offs) == [0, 96, 120, 300] and P.offsets_to_batches(offs) == batches
+    assert len(P.batches_to_offsets([])) == 0 and P.offsets_to_batches(np.array([], dtype=np.int64)) == []
+
+
+def test_hash_config():  # reference tests/test_strategies.py:151-157, :112-124
+    for bad in (dict(table_size=12), dict(multiplier=2), dict(max_fast_probes=0), dict(multiplier=2**32 + 1)):
+        with pytest.raises(ConfigError):
+            HashConfig(**bad)
+    h = HashConfig(table_size=8)
+    assert (h.slot(5), h.slot(7), h.slot(3)) == (0, 2, 6)
+    assert HashConfig(table_size=1).slot(12345) == 0
+
+
+def test_probe_stats_merge():
+    assert ProbeStats(1, 2, 3).merge(ProbeStats(4, 5, 2)) == ProbeStats(5, 7, 3)
+    assert ProbeStats(1, 2, 3).total == 3
+
+
+def test_worker_env_cap(monkeypatch):  # reference tests/test_strategies.py:282-289
+    monkeypatch.setenv("VRLAB_THREADS", "2")
+    assert effective_workers(8) == 2
+    monkeypatch.setenv("VRLAB_THREADS", "junk")
+    with pytest.raises(ConfigError):
+        effective_workers(8)
+    monkeypatch.delenv("VRLAB_THREADS")
+    assert effective_workers(8) == 8
+
+
+def test_warp_primitives():  # reference tests/test_warp.py
+    from paper_1805_08893_b200.warp import WarpState, ballot, ffs, lane_bit, shfl
+    assert shfl(WarpState((1, 2, 3, 4)), 2).lanes == (3, 3, 3, 3)
+    assert ballot([True, False, True]) == 0b101 and ffs(0) == 0 and ffs(0b1000) == 4
+    assert lane_bit(3, 4) == 8 and lane_bit(4, 4) == 0
+    with pytest.raises(ValueError):
+        WarpState((1, 2, 3))
+
+
+def test_mesh_generators_match_oracle_restatement():
+    import oracle as O
+    m = P.gen_grid(9, 13)
+    p, i = O.gen_grid(9, 13)
+    assert np.array_equal(m.positions, p) and np.array_equal(m.indices, i)
+    assert np.array_equal(P.shuffle_triangles(m, 4).indices, O.shuffle_triangles(i, 4))
+    s = P.gen_icosphere(2)
+    assert s.vertex_count == 10 * 16 + 2 and s.triangle_count == 20 * 16
+    np.testing.assert_allclose(np.linalg.norm(s.positions, axis=1), 1.0, atol=1e-12)
+    with pytest.raises(P.MeshError):
+        P.IndexedMesh(positions=np.zeros((2, 3)), indices=np.array([0, 1, 5], dtype=np.uint32))
+
+
+def test_golden_meshes_match_generators(golden_dir):
+    """The corpus of tests/helpers.py:20-40 rebuilt with our generators equals the reference's."""
+    data = np.load(os.path.join(golden_dir, "runs.npz"))
+    rng = np.random.default_rng(100)
+    for i in range(20):
+        kind = i % 4
+        if kind == 0:
+            m = P.gen_grid(int(rng.integers(2, 11)), int(rng.integers(2, 11)))
+        elif kind == 1:
+            m = P.gen_icosphere(int(rng.integers(0, 3)))
+        elif kind == 2:
+            g = P.gen_grid(int(rng.integers(3, 11)), int(rng.integers(3, 11)))
+            m = P.shuffle_triangles(g, int(rng.integers(0, 2**31)))
+        else:
+            s = P.gen_icosphere(int(rng.integers(1, 3)))
+            m = P.shuffle_triangles(s, int(rng.integers(0, 2**31)))
+        assert np.array_equal(m.indices, data[f"m{i}_indices"])
+        assert np.array_equal(m.positions, data[f"m{i}_positions"])
+
+
+def test_build_report_contract():  # reference tests/test_analytics.py:53-60
+    with pytest.raises(AssertionError):
+        P.build_report(scene="s", strategy="naive", indices=6, invocations=6, batches=1,
+                       shade_counts=np.array([1, 1]))
+    rep = P.build_report(scene="s", strategy="sort", indices=9, invocations=3, batches=1)
+    assert rep.reuse_rate == 1 - 3 / 9
+    assert set(rep.to_dict()) == {"scene", "strategy", "indices", "invocations", "reuse_rate", "batches"}
+    assert P.build_report(scene="", strategy="x", indices=0, invocations=0, batches=0).reuse_rate == 0.0
+
+
+# ---- boundary -----------------------------------------------------------------------------
+def test_library_builds_and_exports_every_declared_symbol():
+    build.build()
+    header = open(os.path.join(ROOT, "include", "vrgeom.h")).read()
+    declared = set(re.findall(r"\b(vr_[a-z_]+)\s*\(", header))
+    assert declared, "no entry points parsed from include/vrgeom.h"
+    assert declared == set(_native.exported_symbols())
+    handle = ctypes.CDLL(build.LIB)
+    for name in declared:
+        assert hasattr(handle, name), f"{name} not exported"
+    assert _native.lib().vr_abi_version() == 1
+    assert _native.status_string(5).startswith("hash table full")
+
+
+def test_sass_is_sm100():
+    out = subprocess.run(["cuobjdump", "-lelf", build.build()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_config_checks_through_abi():
+    lib = _native.lib()
+    ok = _native.BatchConfigC(96, 256, 1023, 32, 256, 3)
+    assert lib.vr_check_batch_config(ctypes.byref(ok)) == 0
+    for bad in ((97, 256, 1023, 32, 256, 3), (96, 2, 1023, 32, 256, 3), (96, 256, 1023, 12, 256, 3)):
+        assert lib.vr_check_batch_config(ctypes.byref(_native.BatchConfigC(*bad))) == _native.VR_ERR_BAD_CONFIG
+    assert lib.vr_check_hash_config(ctypes.byref(_native.HashConfigC(12, 3, 8))) == _native.VR_ERR_BAD_CONFIG
+    assert lib.vr_static_batch_count(99, ctypes.byref(ok)) == 2
+
+
+def test_no_cpu_fallback_without_device():
+    """On a box without a GPU every compute entry point refuses loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(_native.NativeLibraryError):
+        P.dynamic_batches(np.array([0, 1, 2], dtype=np.uint32), BatchConfig())
+    with pytest.raises(_native.NativeLibraryError):
+        P.sort_batch(np.array([0, 1, 2], dtype=np.uint32))
+    m = P.gen_grid(3, 3)
+    with pytest.raises(_native.NativeLibraryError):
+        P.run_sorting(m, P.static_batches(len(m.indices), BatchConfig()), BatchConfig(), P.identity_shader())
+
+
+def test_product_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_1805_08893_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in text and "from oracle" not in text, f
+                assert "vr_oracle" not in text, f
+
+
+def test_runner_validation_is_host_side():
+    """Errors the reference raises before touching data need no GPU either."""
+    ids = np.array([0, 1, 2], dtype=np.uint32)
+    with pytest.raises(ConfigError):  # test_strategies.py:293-296
+        P.run_on_indices("magic", ids, [Batch(0, 3)], BatchConfig(), P.identity_shader())
+    with pytest.raises(ConfigError):  # test_strategies.py:298-301
+        P.run_on_indices("naive", ids, [Batch(0, 6)], BatchConfig(), P.identity_shader())
+    with pytest.raises(ConfigError):  # test_strategies.py:303-309
+        P.run_on_indices("hash", ids, [Batch(0, 3)], BatchConfig(max_unique=256), P.identity_shader(),
+                         HashConfig(table_size=128))
+    # empty batch list is legal and needs no device (test_strategies.py:40-45, :183-190)
+    stream, rep = P.run_on_indices("naive", np.array([], dtype=np.uint32), [], BatchConfig(), P.identity_shader())
+    assert rep.invocations == 0 and len(stream) == 0
+    stream, rep, stats = P.run_on_indices("hash", np.array([], dtype=np.uint32), [], BatchConfig(),
+                                          P.identity_shader(), HashConfig())
+    assert len(stream) == 0 and rep.invocations == 0 and stats.total == 0

@@ -1,0 +1,93 @@
+"""N>1 host logic on CPU: world_size-2 gloo processes shard a batch list, each computes its
+shard's statistics with the oracle standing in for the device, and the reduced block must
+equal the single-process result."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1805_08893_b200 import _native as N
+from paper_1805_08893_b200 import shard
+
+
+def test_shard_range_partitions():
+    for n in (0, 1, 7, 224914):
+        for world in (1, 2, 3, 8):
+            cuts = [shard.shard_range(n, r, world) for r in range(world)]
+            assert cuts[0][0] == 0 and cuts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(cuts, cuts[1:]))
+            sizes = [hi - lo for lo, hi in cuts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_shard_batches_whole_batches():
+    offs = np.array([0, 96, 192, 288, 300], dtype=np.int64)
+    parts = [shard.shard_batches(offs, r, 3) for r in range(3)]
+    assert [list(p) for p in parts] == [[0, 96, 192], [192, 288], [288, 300]]
+    assert len(shard.shard_batches(offs[:1], 0, 2)) == 0
+
+
+def test_lpt_assign_balances():
+    sizes = np.array([50, 10, 40, 30, 20, 60, 5])
+    parts = shard.lpt_assign(sizes, 3)
+    assert sorted(np.concatenate(parts).tolist()) == list(range(7))
+    loads = [int(sizes[p].sum()) for p in parts]
+    assert max(loads) - min(loads) <= 15
+    assert all((np.diff(p) > 0).all() for p in parts)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    import oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _, idx = O.gen_grid(40, 40)
+    offs = O.dynamic_batches(idx, max_unique=32, max_indices=127)
+    mine = shard.shard_batches(offs, rank, world)
+    stats = torch.zeros(N.VR_STATS_WORDS, dtype=torch.int64)
+    stats[N.VR_STAT_ERROR] = -1
+    if len(mine):
+        fr = O.run("hash", idx, mine[:-1], mine[1:], max_unique=32, table_size=32)
+        stats[N.VR_STAT_INDICES] = fr.indices
+        stats[N.VR_STAT_INVOCATIONS] = fr.invocations
+        stats[N.VR_STAT_BATCHES] = len(mine) - 1
+        stats[N.VR_STAT_ROUNDS] = fr.rounds
+        stats[N.VR_STAT_PROBES_FAST] = fr.probes_fast
+        stats[N.VR_STAT_PROBE_MAX_CHAIN] = fr.probe_max_chain
+    total = shard.reduce_stats(stats)
+    if rank == 0:
+        q.put(total.tolist())
+    dist.destroy_process_group()
+
+
+def test_two_rank_statistics_match_single_process():
+    import oracle as O
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    total = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    _, idx = O.gen_grid(40, 40)
+    offs = O.dynamic_batches(idx, max_unique=32, max_indices=127)
+    fr = O.run("hash", idx, offs[:-1], offs[1:], max_unique=32, table_size=32)
+    assert total[N.VR_STAT_INDICES] == fr.indices and total[N.VR_STAT_INVOCATIONS] == fr.invocations
+    assert total[N.VR_STAT_BATCHES] == len(offs) - 1 and total[N.VR_STAT_ROUNDS] == fr.rounds
+    assert total[N.VR_STAT_PROBES_FAST] == fr.probes_fast
+    assert total[N.VR_STAT_PROBE_MAX_CHAIN] == fr.probe_max_chain
+    assert total[N.VR_STAT_ERROR] == -1
