@@ -46,6 +46,10 @@ enum vr_strategy {
  * (strategies.py:235-298 have no unique budget; the guards of strategies.py:432-435 and
  * :451-455 belong to run_on_indices). */
 #define VR_FLAG_NO_BUDGET 0x100
+/* OR into `strategy` when the batches tile one range of the buffer in order
+ * (batch_end[b] == batch_begin[b+1], e.g. any offsets array of batching.py:128-137):
+ * the span scan is skipped.  The kernels verify the claim and report VR_ERR_BAD_BATCH. */
+#define VR_FLAG_CONTIGUOUS 0x200
 
 enum vr_status {
     VR_OK = 0,
@@ -183,10 +187,10 @@ int vr_expand_stream(const int32_t *d_batch_round_off, const int32_t *d_round_ui
                      size_t workspace_bytes, void *stream);
 
 /* Profiling aid (bench.py): per-kernel device time of the last vr_run, measured with CUDA
- * events on the launching stream.  Stages, in order: span scan, dedup, count scan,
- * shade/finalize, statistics.  Process-wide; do not enable under concurrent vr_run calls.
+ * events on the launching stream.  Stages, in order: init (+ span scan), dedup, offset scan
+ * (+ statistics), shade/finalize.  Process-wide; do not enable under concurrent vr_run calls.
  * vr_profile_read synchronises the last event and returns the number of stages written. */
-#define VR_PROFILE_STAGES 5
+#define VR_PROFILE_STAGES 4
 int vr_profile_enable(int on);
 int vr_profile_read(float *ms, int cap);
 

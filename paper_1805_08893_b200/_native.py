@@ -16,14 +16,15 @@ STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_
  VR_ERR_UNSUPPORTED, VR_ERR_CUDA, VR_ERR_CAPACITY, VR_ERR_WORKSPACE, VR_ERR_PRIM_OVER_BUDGET) = range(15)
 
 VR_FLAG_NO_BUDGET = 0x100
+VR_FLAG_CONTIGUOUS = 0x200
 
 VR_SHADER_NONE, VR_SHADER_IDENTITY, VR_SHADER_POSITION = range(3)
 
 (VR_STAT_INDICES, VR_STAT_INVOCATIONS, VR_STAT_BATCHES, VR_STAT_ROUNDS, VR_STAT_PROBES_FAST,
  VR_STAT_PROBES_SLOW, VR_STAT_PROBE_MAX_CHAIN, VR_STAT_ERROR) = range(8)
 VR_STATS_WORDS = 16
-VR_PROFILE_STAGES = 5
-PROFILE_STAGE_NAMES = ("span_scan", "dedup", "count_scan", "shade_finalize", "stats")
+VR_PROFILE_STAGES = 4
+PROFILE_STAGE_NAMES = ("init", "dedup", "offset_scan", "shade_finalize")
 
 
 class NativeLibraryError(RuntimeError):

@@ -28,14 +28,6 @@ __host__ __device__ inline int ilog2(uint32_t pow2) {
     return b;
 }
 
-// First failing batch wins, as in the reference's in-order loop (strategies.py:470):
-// word = (batch << 8) | status, reduced with a signed 64-bit min; -1 == clean is
-// stored as INT64_MAX internally and rewritten by the finalize kernel.
-__device__ inline void report_error(int64_t* stats, int64_t batch, int status) {
-    long long word = (long long)((batch << 8) | (int64_t)status);
-    atomicMin((long long*)&stats[VR_STAT_ERROR], word);
-}
-
 // strategies.py:88-91 HashConfig.slot; bits == 0 (table_size 1) -> slot 0.
 __device__ __forceinline__ uint32_t hash_slot(uint32_t vid, uint32_t mult, int bits) {
     uint32_t prod = vid * mult;

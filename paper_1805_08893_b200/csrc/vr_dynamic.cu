@@ -237,7 +237,12 @@ static DynLayout dyn_layout(int64_t n, const vr_batch_config* cfg) {
     int tile = (L.window + 31) & ~31;
     if (tile < 1024) tile = 1024;
     L.tile = tile;
-    L.slots = (int)next_pow2((uint32_t)(2 * (tile + ((L.window + 31) & ~31) + 32)));
+    {   // distinct ids seen by one warp <= tile + halo; keep the table load below ~0.67
+        const int cnt = tile + ((L.window + 31) & ~31) + 32;
+        int slots = (int)next_pow2((uint32_t)cnt);
+        if (2 * slots < 3 * cnt) slots <<= 1;
+        L.slots = slots;
+    }
     size_t o = 0;
     L.prev = o; o += al((size_t)n * 4 + 64);
     L.nxt = o; o += al((size_t)n * 4 + 64);

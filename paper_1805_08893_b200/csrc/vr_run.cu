@@ -1,19 +1,22 @@
 // vr_run.cu -- per-batch dedup kernels, shading/assembly and the vr_run entry point.
 //
-// Pipeline of one vr_run call (all on the caller's stream, no host sync):
-//   K0 span_scan     exclusive scan of batch spans -> position of every batch in the
-//                    concatenated assembly map; validates the ranges
-//                    (strategies.py:426-428)
-//   K1 dedup_*       one thread group per batch: the strategy's dedup
-//                    (strategies.py:159-298) -> assembly map (final), unique ids and
-//                    round records (staged), per-batch (rounds, invocations)
-//   K2 count_scan    exclusive scan of (rounds, invocations) -> output offsets, totals,
-//                    statistics (strategies.py:472-483)
-//   K3 finalize      unique ids to their final place + vertex shader once per unique id
-//                    (strategies.py:456-463) + per-vertex tally (strategies.py:485-489)
+// Pipeline of one vr_run call (all on the caller's stream, no host synchronisation):
+//   K0 init          clears the accumulators; for NON-contiguous batch lists also the scan of
+//                    batch spans that places every batch in the concatenated assembly map
+//   K1 dedup_*       one thread / CTA per batch: validation (strategies.py:426-428) and the
+//                    strategy's dedup (strategies.py:159-298) -> assembly map (final), unique
+//                    ids and round records (staged), per-batch (rounds, invocations)
+//   K2 tile_reduce + tile_scan
+//                    two-level exclusive scan of (rounds, invocations) over tiles of batches
+//                    -> output offsets, totals, statistics (strategies.py:472-483)
+//   K3 finalize      one CTA per tile: round tables and unique ids to their final offsets and
+//                    the vertex shader once per unique id (strategies.py:456-463), 16-byte
+//                    gathers / coalesced 16-byte stores, optional per-vertex tally (:485-489)
 #include "vr_common.cuh"
 
 namespace vr {
+
+enum { ACC_PROBES_FAST = 0, ACC_PROBES_SLOW, ACC_MAX_CHAIN, ACC_ERROR, ACC_ABORT, ACC_WORDS = 8 };
 
 struct RunCtx {
     const uint32_t* __restrict__ idx;
@@ -29,21 +32,33 @@ struct RunCtx {
     uint32_t multiplier;
     int table_bits;
     int enforce_budget;  // strategies.py:451-455 applies to sort/hash/phash
-    int stage_factor;    // staged unique ids per batch <= span * stage_factor + ps
+    int stage_factor;    // staged unique ids per batch <= span * stage_factor
+    int contiguous;      // batches tile [bbegin[0], bend[n-1]) in order: map offset = begin - first
+    int tile_batches;    // batches per scan / finalize tile
+    int n_tiles;
+    int64_t span_cap;    // caller's bound on the sum of batch spans
     // workspace
-    int32_t* map_off;      // [n_batches+1]
-    int2* counts;          // [n_batches] (rounds, invocations)
-    int32_t* uid_off;      // [n_batches+1]
-    int32_t* round_off;    // [n_batches+1]
-    int64_t span_cap;      // caller's bound on the sum of batch spans
-    uint32_t* stage_uid;   // staged unique ids
-    int32_t* stage_rn;     // staged per-round claim counts (warp)
-    int32_t* stage_rp;     // staged per-round primitives (warp)
-    int32_t* flags;        // [0] abort
+    int32_t* map_off;       // [n_batches+1] (non-contiguous lists only)
+    int2* counts;           // [n_batches] (rounds, invocations)
+    int2* tile_sums;        // [n_tiles]
+    int2* tile_base;        // [n_tiles+1] exclusive prefix of tile_sums
+    uint32_t* stage_uid;    // staged unique ids
+    uint32_t* stage_round;  // staged round records: primitives << 8 | claims (warp)
+    long long* acc;         // [ACC_WORDS]
     // outputs
     vr_outputs out;
 };
 
+// First failing batch wins, as in the reference's in-order loop (strategies.py:470):
+// the accumulator starts at 0 and takes the max of ((2^47-1 - batch) << 8 | status).
+__device__ inline void report_error(const RunCtx& c, int64_t batch, int status) {
+    long long word = (long long)(((0x7FFFFFFFFFFFLL - batch) << 8) | (long long)status);
+    atomicMax(&c.acc[ACC_ERROR], word);
+}
+
+__device__ __forceinline__ int batch_map_off(const RunCtx& c, int b, int begin) {
+    return c.contiguous ? begin - __ldg(c.bbegin) : c.map_off[b];
+}
 __device__ __forceinline__ int64_t stage_uid_base(const RunCtx& c, int b, int mo) {
     return (int64_t)mo * c.stage_factor + (int64_t)b * c.ps;
 }
@@ -51,49 +66,52 @@ __device__ __forceinline__ int64_t stage_round_base(const RunCtx& c, int b, int 
     return (int64_t)mo / c.ps + b;
 }
 
+// strategies.py:427: 0 <= begin < end <= len(idx) and span % ps == 0 (+ device limits).
+__device__ __forceinline__ bool validate_batch(const RunCtx& c, int b, int& begin, int& span) {
+    const int bg = __ldg(c.bbegin + b), en = __ldg(c.bend + b);
+    begin = bg;
+    span = en - bg;
+    bool ok = bg >= 0 && bg < en && (int64_t)en <= c.n_idx && (span % c.ps) == 0;
+    if (ok && c.contiguous && b + 1 < c.n_batches) ok = __ldg(c.bbegin + b + 1) == en;
+    if (!ok) { report_error(c, b, VR_ERR_BAD_BATCH); return false; }
+    if (span > c.max_span) { report_error(c, b, VR_ERR_UNSUPPORTED); return false; }
+    return true;
+}
+
 // ---------------------------------------------------------------------------------
-// K0: spans -> map_off (single CTA, strided chunks).  Also initialises the statistics.
+// K0
 // ---------------------------------------------------------------------------------
+__global__ void init_kernel(RunCtx c) {
+    if (threadIdx.x < ACC_WORDS) c.acc[threadIdx.x] = 0;
+}
+
+// Non-contiguous batch lists: single-CTA scan of the spans (general path, not the hot one).
 __global__ void __launch_bounds__(1024) span_scan_kernel(RunCtx c) {
     __shared__ int scratch[40];
     __shared__ int chunk[1024];
     __shared__ long long carry;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        carry = 0;
-        for (int i = 0; i < VR_STATS_WORDS; i++) c.out.d_stats[i] = 0;
-        c.out.d_stats[VR_STAT_ERROR] = 0x7fffffffffffffffLL;
-        c.flags[0] = 0;
-    }
+    if (tid == 0) carry = 0;
     __syncthreads();
     for (int base = 0; base < c.n_batches; base += 1024) {
         int b = base + tid;
         int span = 0;
         if (b < c.n_batches) {
             int bg = c.bbegin[b], en = c.bend[b];
-            // strategies.py:427: 0 <= begin < end <= len(idx) and span % ps == 0
-            bool ok = bg >= 0 && bg < en && (int64_t)en <= c.n_idx && ((en - bg) % c.ps) == 0;
-            if (!ok) report_error(c.out.d_stats, b, VR_ERR_BAD_BATCH);
-            else if (en - bg > c.max_span) report_error(c.out.d_stats, b, VR_ERR_UNSUPPORTED);
-            else span = en - bg;
+            if (bg >= 0 && bg < en && (int64_t)en <= c.n_idx) span = en - bg;  // K1 reports the bad ones
         }
         chunk[tid] = span;
         __syncthreads();
         int total = block_exclusive_scan(chunk, 1024, scratch);
         long long cbase = carry;
-        if (b < c.n_batches) {
-            long long off = cbase + chunk[tid];
-            c.map_off[b] = (int32_t)off;
-        }
+        if (b < c.n_batches) c.map_off[b] = (int32_t)min(cbase + chunk[tid], 0x7fffffffLL);
         __syncthreads();
         if (tid == 0) carry = cbase + total;
         __syncthreads();
     }
     if (tid == 0) {
-        c.map_off[c.n_batches] = (int32_t)carry;
-        if (carry > 0x7fffffffLL) report_error(c.out.d_stats, 0, VR_ERR_UNSUPPORTED);
-        else if (carry > c.span_cap) report_error(c.out.d_stats, 0, VR_ERR_CAPACITY);
-        if (c.out.d_stats[VR_STAT_ERROR] != 0x7fffffffffffffffLL) c.flags[0] = 1;  // abort K1..K3
+        c.map_off[c.n_batches] = (int32_t)min((long long)carry, 0x7fffffffLL);
+        if (carry > c.span_cap) { report_error(c, 0, VR_ERR_CAPACITY); c.acc[ACC_ABORT] = 1; }
     }
 }
 
@@ -101,70 +119,140 @@ __global__ void __launch_bounds__(1024) span_scan_kernel(RunCtx c) {
 // K1 (naive): strategies.py:159-170 -- one round per primitive, no reuse.  Closed form:
 // nothing to stage, the finalize kernel reads the index buffer directly.
 // ---------------------------------------------------------------------------------
-__global__ void naive_counts_kernel(RunCtx c) {
+__global__ void __launch_bounds__(256) naive_counts_kernel(RunCtx c) {
     int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= c.n_batches || c.flags[0]) return;
-    int span = c.map_off[b + 1] - c.map_off[b];
+    if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
+    int begin, span;
+    if (!validate_batch(c, b, begin, span)) { c.counts[b] = make_int2(0, 0); return; }
     c.counts[b] = make_int2(span / c.ps, span);
 }
 
 // ---------------------------------------------------------------------------------
-// K1 (warp voting), generic path: strategies.py:173-232 in closed form, one thread per
-// batch, any warp_width in {4,8,16,32,64} and any batch size.
+// K1 (warp voting): strategies.py:173-232 in closed form, one THREAD per batch.
 //
 // Per round over the not yet consumed ids v[cursor..n):
 //   claims   = distinct values in first-occurrence order (Algorithm 1 assigns each new id
-//              to the lowest free lane, strategies.py:207-212), at most w of them;
-//   the round stops at the first value that would be the (w+1)-th distinct one
-//   (outgoing == 0, strategies.py:220), or at the end of the w-wide fetch in which the
-//   w-th claim was made (loop condition fill < w, strategies.py:201), or at the batch end
+//              to the lowest free lane, strategies.py:207-212), at most W of them;
+//   the round stops at the first value that would be the (W+1)-th distinct one
+//   (outgoing == 0, strategies.py:220), or at the end of the W-wide fetch in which the
+//   W-th claim was made (loop condition fill < W, strategies.py:201), or at the batch end
 //   (sentinel lanes, strategies.py:202,220);
 //   primitives emitted = done // ps, cursor += emitted * ps (strategies.py:225-231);
 //   every claim is shaded, including those only referenced by the discarded tail.
+//
+// The lock-step lanes of Algorithm 1 are the claim slots; on the B200 the 32 batches of a
+// warp advance together instead.  Each thread streams its batch with 16-byte loads (one
+// prefetched ahead), looks ids up in a private 2W-slot open-addressing table in shared
+// memory ([slot][thread] layout: bank == lane, conflict-free; entries are tagged with the
+// round number so nothing is cleared between rounds), stages claims and round records,
+// and writes local indices 8 at a time as one 16-byte store from a 16-entry ring.
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) warp_generic_kernel(RunCtx c) {
-    int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= c.n_batches || c.flags[0]) return;
-    const int begin = c.bbegin[b];
-    const int mo = c.map_off[b];
-    const int n = c.map_off[b + 1] - mo;
-    const int w = c.warp_width, ps = c.ps;
-    const uint32_t* __restrict__ ids = c.idx + begin;
+constexpr int kTpbThreads = 128;
+
+template <int W>
+__global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
+    constexpr int S = 2 * W;  // table slots per thread
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);                 // [S][T]
+    uint32_t* ring = keys + S * kTpbThreads;                                // [16][T]
+    uint16_t* tags = reinterpret_cast<uint16_t*>(ring + 16 * kTpbThreads);  // [S][T] tag<<6 | rank
+    const int t = threadIdx.x;
+    const int b = blockIdx.x * kTpbThreads + t;
+#pragma unroll
+    for (int h = 0; h < S; h++) tags[h * kTpbThreads + t] = 0xFFFFu;
+    if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
+    int begin, n;
+    if (!validate_batch(c, b, begin, n)) { c.counts[b] = make_int2(0, 0); return; }
+    const int mo = batch_map_off(c, b, begin);
+    const int ps = c.ps;
     uint16_t* __restrict__ amap = c.out.d_assembly_map ? c.out.d_assembly_map + mo : nullptr;
+    const bool amap_vec = (mo & 7) == 0;
     uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
-    int32_t* __restrict__ srn = c.stage_rn + stage_round_base(c, b, mo);
-    int32_t* __restrict__ srp = c.stage_rp + stage_round_base(c, b, mo);
-    uint32_t claims[64];
-    int cursor = 0, rounds = 0, inv = 0;
+    uint32_t* __restrict__ srd = c.stage_round + stage_round_base(c, b, mo);
+    const uint4* __restrict__ quads = reinterpret_cast<const uint4*>(c.idx);
+    const int64_t n_quads_full = c.n_idx >> 2;  // quads that lie completely inside the buffer
+
+    auto load_quad = [&](int64_t gq) -> uint4 {
+        if (gq < n_quads_full) return __ldg(quads + gq);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        const int64_t g = gq << 2;
+        if (g + 0 < c.n_idx) v.x = __ldg(c.idx + g + 0);
+        if (g + 1 < c.n_idx) v.y = __ldg(c.idx + g + 1);
+        if (g + 2 < c.n_idx) v.z = __ldg(c.idx + g + 2);
+        return v;
+    };
+    int64_t cq = ((int64_t)begin) >> 2;
+    uint4 cur = load_quad(cq), nxt = load_quad(cq + 1);
+
+    auto flush_group = [&](int g, int count) {
+        if (!amap) return;
+        uint32_t r[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = ring[((8 * g + j) & 15) * kTpbThreads + t];
+        if (count == 8 && amap_vec) {
+            uint4 v = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), r[4] | (r[5] << 16), r[6] | (r[7] << 16));
+            *reinterpret_cast<uint4*>(amap + 8 * g) = v;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++)
+                if (j < count) amap[8 * g + j] = (uint16_t)r[j];
+        }
+    };
+
+    int cursor = 0, rounds = 0, inv = 0, flushed = 0;
+    uint32_t tagno = 0;
+    bool failed = false;
     while (cursor < n) {
         int fill = 0, stop = n, done;
         int i = cursor;
-        for (;; i++) {
+        for (;;) {
             if (i >= stop) { done = stop; break; }
-            uint32_t x = ids[i];
+            const int64_t g = (int64_t)begin + i;
+            const int64_t gq = g >> 2;
+            if (gq != cq) {
+                cur = (gq == cq + 1) ? nxt : load_quad(gq);
+                cq = gq;
+                nxt = load_quad(gq + 1);
+            }
+            const int lane4 = (int)(g & 3);
+            const uint32_t x = lane4 == 0 ? cur.x : lane4 == 1 ? cur.y : lane4 == 2 ? cur.z : cur.w;
+            uint32_t h = (x ^ (x >> 7) ^ (x >> 13)) & (S - 1);
             int r = -1;
-            for (int k = 0; k < fill; k++)
-                if (claims[k] == x) { r = k; break; }
+            for (;;) {
+                const uint32_t tg = tags[h * kTpbThreads + t];
+                if ((tg >> 6) != tagno) break;  // free: never used or left over from an earlier round
+                if (keys[h * kTpbThreads + t] == x) { r = (int)(tg & 63u); break; }
+                h = (h + 1) & (S - 1);
+            }
             if (r < 0) {
-                if (fill >= w) { done = i; break; }  // first unassignable slot
-                claims[fill] = x;
+                if (fill >= W) { done = i; break; }  // first unassignable slot
+                keys[h * kTpbThreads + t] = x;
+                tags[h * kTpbThreads + t] = (uint16_t)((tagno << 6) | (uint32_t)fill);
                 suid[inv + fill] = x;
                 r = fill++;
-                if (fill == w) stop = min(n, cursor + ((i - cursor) / w + 1) * w);
+                if (fill == W) stop = min(n, cursor + ((i - cursor) / W + 1) * W);
             }
-            if (amap) amap[i] = (uint16_t)r;
+            ring[(i & 15) * kTpbThreads + t] = (uint32_t)r;
+            if (i >= 8 * flushed + 10) { flush_group(flushed, 8); flushed++; }  // positions <= i-3 are final
+            i++;
         }
-        int emitted = (done - cursor) / ps;
-        if (emitted == 0) {  // strategies.py:226-227 (unreachable for w >= ps)
-            report_error(c.out.d_stats, b, VR_ERR_WARP_NO_PROGRESS);
+        const int emitted = (done - cursor) / ps;
+        if (emitted == 0) {  // strategies.py:226-227 (unreachable for W >= ps)
+            report_error(c, b, VR_ERR_WARP_NO_PROGRESS);
+            failed = true;
             break;
         }
-        srn[rounds] = fill;
-        srp[rounds] = emitted;
+        srd[rounds] = ((uint32_t)emitted << 8) | (uint32_t)fill;
         rounds++;
         inv += fill;
         cursor += emitted * ps;
+        if (++tagno == 1023u) {  // tag space exhausted: wipe this thread's column
+            for (int h = 0; h < S; h++) tags[h * kTpbThreads + t] = 0xFFFFu;
+            tagno = 0;
+        }
     }
+    if (failed) { c.counts[b] = make_int2(0, 0); return; }
+    for (int g = flushed; 8 * g < n; g++) flush_group(g, min(8, n - 8 * g));
     c.counts[b] = make_int2(rounds, inv);
 }
 
@@ -181,11 +269,14 @@ __global__ void __launch_bounds__(256) sort_batch_kernel(RunCtx c, int pmax) {
     uint16_t* maps = reinterpret_cast<uint16_t*>(heads + pmax);
     __shared__ int scratch[40];
     const int b = blockIdx.x;
-    if (c.flags[0]) return;
+    if (c.acc[ACC_ABORT]) return;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int begin = c.bbegin[b];
-    const int mo = c.map_off[b];
-    const int n = c.map_off[b + 1] - mo;
+    int begin, n;
+    if (!validate_batch(c, b, begin, n)) {  // uniform: every thread evaluates the same values
+        if (tid == 0) c.counts[b] = make_int2(0, 0);
+        return;
+    }
+    const int mo = batch_map_off(c, b, begin);
     const int P = (int)next_pow2((uint32_t)max(n, 2));
     const uint32_t* __restrict__ ids = c.idx + begin;
     for (int i = tid; i < P; i += nt)
@@ -221,7 +312,7 @@ __global__ void __launch_bounds__(256) sort_batch_kernel(RunCtx c, int pmax) {
         for (int i = tid; i < n; i += nt) c.out.d_assembly_map[mo + i] = maps[i];
     if (tid == 0) {
         c.counts[b] = make_int2(1, nu);
-        if (c.enforce_budget && nu > c.max_unique) report_error(c.out.d_stats, b, VR_ERR_OVER_BUDGET);
+        if (c.enforce_budget && nu > c.max_unique) report_error(c, b, VR_ERR_OVER_BUDGET);
     }
 }
 
@@ -253,11 +344,14 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
     __shared__ int s_unique, s_chain_max;
     __shared__ unsigned long long s_chain_sum;
     const int b = blockIdx.x;
-    if (c.flags[0]) return;
+    if (c.acc[ACC_ABORT]) return;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int begin = c.bbegin[b];
-    const int mo = c.map_off[b];
-    const int n = c.map_off[b + 1] - mo;
+    int begin, n;
+    if (!validate_batch(c, b, begin, n)) {
+        if (tid == 0) c.counts[b] = make_int2(0, 0);
+        return;
+    }
+    const int mo = batch_map_off(c, b, begin);
     const uint32_t tsize = c.table_size, tmask = tsize - 1;
     const uint32_t qmask = (uint32_t)q - 1;
     const int qbits = ilog2((uint32_t)q);
@@ -290,8 +384,8 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
     const int nu = s_unique;
     if (nu > (int)tsize) {  // strategies.py:283-284: chain would exceed table_size
         if (tid == 0) {
-            report_error(c.out.d_stats, b, VR_ERR_HASH_FULL);
-            c.counts[b] = make_int2(1, 0);
+            report_error(c, b, VR_ERR_HASH_FULL);
+            c.counts[b] = make_int2(0, 0);
         }
         return;
     }
@@ -341,76 +435,85 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
         for (int i = tid; i < n; i += nt) c.out.d_assembly_map[mo + i] = maps[i];
     if (tid == 0) {
         c.counts[b] = make_int2(1, nu);
-        atomicAdd((unsigned long long*)&c.out.d_stats[VR_STAT_PROBES_FAST], s_chain_sum);
-        atomicMax((long long*)&c.out.d_stats[VR_STAT_PROBE_MAX_CHAIN], (long long)s_chain_max);
-        if (c.enforce_budget && nu > c.max_unique) report_error(c.out.d_stats, b, VR_ERR_OVER_BUDGET);
+        atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], s_chain_sum);
+        atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)s_chain_max);
+        if (c.enforce_budget && nu > c.max_unique) report_error(c, b, VR_ERR_OVER_BUDGET);
     }
 }
 
 // ---------------------------------------------------------------------------------
-// K2: exclusive scan of per-batch (rounds, invocations); totals and statistics.
+// K2: two-level exclusive scan of per-batch (rounds, invocations).
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) count_scan_kernel(RunCtx c) {
+__global__ void __launch_bounds__(128) tile_reduce_kernel(RunCtx c) {
+    __shared__ int sr[4], su[4];
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int b0 = tile * c.tile_batches, b1 = min(c.n_batches, b0 + c.tile_batches);
+    int r = 0, u = 0;
+    for (int b = b0 + tid; b < b1; b += 128) { int2 v = c.counts[b]; r += v.x; u += v.y; }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, d);
+        u += __shfl_xor_sync(0xffffffffu, u, d);
+    }
+    if ((tid & 31) == 0) { sr[tid >> 5] = r; su[tid >> 5] = u; }
+    __syncthreads();
+    if (tid == 0) c.tile_sums[tile] = make_int2(sr[0] + sr[1] + sr[2] + sr[3], su[0] + su[1] + su[2] + su[3]);
+}
+
+__global__ void __launch_bounds__(1024) tile_scan_kernel(RunCtx c) {
     __shared__ int scratch[40];
     __shared__ int chunk_r[1024];
     __shared__ int chunk_u[1024];
     __shared__ long long carry_r, carry_u;
     const int tid = threadIdx.x;
-    if (c.flags[0]) {
-        if (tid == 0) {
-            c.out.d_stats[VR_STAT_BATCHES] = c.n_batches;
-        }
-        return;
-    }
     if (tid == 0) { carry_r = 0; carry_u = 0; }
     __syncthreads();
-    for (int base = 0; base < c.n_batches; base += 1024) {
-        int b = base + tid;
-        int2 v = b < c.n_batches ? c.counts[b] : make_int2(0, 0);
+    for (int base = 0; base < c.n_tiles; base += 1024) {
+        int k = base + tid;
+        int2 v = k < c.n_tiles ? c.tile_sums[k] : make_int2(0, 0);
         chunk_r[tid] = v.x;
         chunk_u[tid] = v.y;
         __syncthreads();
         int tr = block_exclusive_scan(chunk_r, 1024, scratch);
         int tu = block_exclusive_scan(chunk_u, 1024, scratch);
         long long br = carry_r, bu = carry_u;
-        if (b < c.n_batches) {
-            c.round_off[b] = (int32_t)(br + chunk_r[tid]);
-            if (c.out.d_batch_round_off) c.out.d_batch_round_off[b] = (int32_t)(br + chunk_r[tid]);
-            c.uid_off[b] = (int32_t)(bu + chunk_u[tid]);
-        }
+        if (k < c.n_tiles)
+            c.tile_base[k] = make_int2((int)min(br + chunk_r[tid], 0x7fffffffLL), (int)min(bu + chunk_u[tid], 0x7fffffffLL));
         __syncthreads();
         if (tid == 0) { carry_r = br + tr; carry_u = bu + tu; }
         __syncthreads();
     }
     if (tid == 0) {
-        long long R = carry_r, U = carry_u;
-        c.round_off[c.n_batches] = (int32_t)R;
-        if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
-        c.uid_off[c.n_batches] = (int32_t)U;
+        const long long R = carry_r, U = carry_u;
+        c.tile_base[c.n_tiles] = make_int2((int)min(R, 0x7fffffffLL), (int)min(U, 0x7fffffffLL));
         int64_t* st = c.out.d_stats;
-        st[VR_STAT_INDICES] = c.map_off[c.n_batches];
+        for (int i = 0; i < VR_STATS_WORDS; i++) st[i] = 0;
+        long long span_total = 0;
+        if (c.n_batches > 0)
+            span_total = c.contiguous ? (long long)c.bend[c.n_batches - 1] - c.bbegin[0] : c.map_off[c.n_batches];
+        if (span_total > c.span_cap) report_error(c, 0, VR_ERR_CAPACITY);
+        if (U > c.out.cap_unique || R > c.out.cap_rounds || U > 0x7fffffffLL) report_error(c, 0, VR_ERR_CAPACITY);
+        st[VR_STAT_INDICES] = span_total;
         st[VR_STAT_INVOCATIONS] = U;
         st[VR_STAT_BATCHES] = c.n_batches;
         st[VR_STAT_ROUNDS] = R;
-        if (U > c.out.cap_unique || R > c.out.cap_rounds || U > 0x7fffffffLL) {
-            report_error(st, 0, VR_ERR_CAPACITY);
-            c.flags[0] = 1;
-        } else if (c.out.d_round_uid_off) {
-            c.out.d_round_uid_off[R] = (int32_t)U;
+        st[VR_STAT_PROBES_FAST] = c.acc[ACC_PROBES_FAST];
+        st[VR_STAT_PROBES_SLOW] = c.acc[ACC_PROBES_SLOW];
+        st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
+        const long long e = c.acc[ACC_ERROR];
+        if (e == 0) {
+            st[VR_STAT_ERROR] = -1;
+            if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
+            if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
+        } else {
+            st[VR_STAT_ERROR] = ((0x7FFFFFFFFFFFLL - (e >> 8)) << 8) | (e & 0xFF);
+            c.acc[ACC_ABORT] = 1;  // K3 must not touch the outputs
         }
     }
 }
 
-__global__ void finish_stats_kernel(RunCtx c) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        if (c.out.d_stats[VR_STAT_ERROR] == 0x7fffffffffffffffLL) c.out.d_stats[VR_STAT_ERROR] = -1;
-    }
-}
-
 // ---------------------------------------------------------------------------------
-// K3: one warp per batch.  Round records and unique ids move to their final offsets; the
-// vertex shader runs once per unique id (strategies.py:456-460) with 16-byte gathers and
-// 16-byte coalesced stores; optional attribute pass-through and per-vertex tally.
+// K3: one CTA per tile of batches.
 // ---------------------------------------------------------------------------------
 __device__ __forceinline__ void shade_one(const RunCtx& c, const ShaderParams& sp, int64_t dst, uint32_t uid) {
     if (c.out.d_unique_ids) c.out.d_unique_ids[dst] = uid;
@@ -422,53 +525,83 @@ __device__ __forceinline__ void shade_one(const RunCtx& c, const ShaderParams& s
     if (c.out.d_shade_counts) atomicAdd(&c.out.d_shade_counts[uid], 1);
 }
 
+constexpr int kFinThreads = 256;
+constexpr int kMaxTile = 1024;
+
 template <int STRATEGY>
-__global__ void __launch_bounds__(256) finalize_kernel(RunCtx c, ShaderParams sp) {
-    const int lane = threadIdx.x & 31;
-    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    if (b >= c.n_batches || c.flags[0]) return;
-    const int mo = c.map_off[b];
-    const int span = c.map_off[b + 1] - mo;
-    const int u0 = c.uid_off[b];
-    const int nu = c.uid_off[b + 1] - u0;
-    if (STRATEGY == VR_NAIVE) {
-        const uint32_t* __restrict__ ids = c.idx + c.bbegin[b];
-        const int ps = c.ps;
-        for (int k = lane; k < span; k += 32) {
-            shade_one(c, sp, (int64_t)u0 + k, ids[k]);
-            if (c.out.d_assembly_map) c.out.d_assembly_map[mo + k] = (uint16_t)(k % ps);
-        }
-        const int r0 = mo / ps;
-        for (int r = lane; r < span / ps; r += 32) {
-            if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0 + r] = u0 + r * ps;
-            if (c.out.d_round_prims) c.out.d_round_prims[r0 + r] = 1;
-        }
-        return;
+__global__ void __launch_bounds__(kFinThreads) finalize_kernel(RunCtx c, ShaderParams sp) {
+    __shared__ int scratch[40];
+    __shared__ int uoff[kMaxTile + 1];  // tile-local exclusive offsets of unique ids
+    __shared__ int roff[kMaxTile + 1];  // tile-local exclusive offsets of rounds
+    if (c.acc[ACC_ABORT]) return;
+    const int tid = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int b0 = tile * c.tile_batches;
+    const int nb = min(c.n_batches, b0 + c.tile_batches) - b0;
+    for (int i = tid; i < nb; i += kFinThreads) {
+        int2 v = c.counts[b0 + i];
+        roff[i] = v.x;
+        uoff[i] = v.y;
     }
-    const int r0 = c.round_off[b];
-    if (STRATEGY == VR_WARP) {
-        const int nr = c.round_off[b + 1] - r0;
-        const int32_t* srn = c.stage_rn + stage_round_base(c, b, mo);
-        const int32_t* srp = c.stage_rp + stage_round_base(c, b, mo);
-        int run = u0;
-        for (int base = 0; base < nr; base += 32) {
-            int r = base + lane;
-            int cnt = r < nr ? srn[r] : 0;
-            int inc = warp_incl_scan(cnt, lane);
-            if (r < nr) {
-                if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0 + r] = run + inc - cnt;
-                if (c.out.d_round_prims) c.out.d_round_prims[r0 + r] = srp[r];
+    __syncthreads();
+    const int tile_rounds = block_exclusive_scan(roff, nb, scratch);
+    const int tile_inv = block_exclusive_scan(uoff, nb, scratch);
+    if (tid == 0) { roff[nb] = tile_rounds; uoff[nb] = tile_inv; }
+    __syncthreads();
+    const int2 base = c.tile_base[tile];
+    const int ps = c.ps;
+    // round tables
+    for (int i = tid; i < nb; i += kFinThreads) {
+        const int b = b0 + i;
+        const int r0 = base.x + roff[i], u0 = base.y + uoff[i];
+        if (c.out.d_batch_round_off) c.out.d_batch_round_off[b] = r0;
+        if (STRATEGY == VR_WARP) {
+            const int begin = __ldg(c.bbegin + b);
+            const int mo = batch_map_off(c, b, begin);
+            const uint32_t* srd = c.stage_round + stage_round_base(c, b, mo);
+            const int nr = roff[i + 1] - roff[i];
+            int run = u0;
+            for (int r = 0; r < nr; r++) {
+                const uint32_t w = srd[r];
+                if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0 + r] = run;
+                if (c.out.d_round_prims) c.out.d_round_prims[r0 + r] = (int)(w >> 8);
+                run += (int)(w & 0xFFu);
             }
-            run += __shfl_sync(0xffffffffu, inc, 31);
-        }
-    } else {
-        if (lane == 0) {
-            if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0] = u0;
-            if (c.out.d_round_prims) c.out.d_round_prims[r0] = span / c.ps;
+        } else if (STRATEGY != VR_NAIVE) {
+            if (roff[i + 1] > roff[i]) {
+                const int span = __ldg(c.bend + b) - __ldg(c.bbegin + b);
+                if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0] = u0;
+                if (c.out.d_round_prims) c.out.d_round_prims[r0] = span / ps;
+            }
         }
     }
-    const uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
-    for (int k = lane; k < nu; k += 32) shade_one(c, sp, (int64_t)u0 + k, suid[k]);
+    if (STRATEGY == VR_NAIVE) {  // one round per primitive: closed form over the tile's rounds
+        for (int r = tid; r < tile_rounds; r += kFinThreads) {
+            if (c.out.d_round_uid_off) c.out.d_round_uid_off[base.x + r] = base.y + r * ps;
+            if (c.out.d_round_prims) c.out.d_round_prims[base.x + r] = 1;
+        }
+    }
+    // unique ids + shading: flat over the tile's outputs, batch found by bisection in smem
+    int steps = 0;
+    while ((1 << steps) < nb) steps++;
+    for (int j = tid; j < tile_inv; j += kFinThreads) {
+        int lo = 0;  // largest i with uoff[i] <= j
+        for (int s = steps - 1; s >= 0; s--) {
+            const int mid = lo + (1 << s);
+            if (mid < nb && uoff[mid] <= j) lo = mid;
+        }
+        const int b = b0 + lo;
+        const int k = j - uoff[lo];
+        const int begin = __ldg(c.bbegin + b);
+        uint32_t uid;
+        if (STRATEGY == VR_NAIVE) {
+            uid = __ldg(c.idx + begin + k);
+            if (c.out.d_assembly_map) c.out.d_assembly_map[batch_map_off(c, b, begin) + k] = (uint16_t)(k % ps);
+        } else {
+            uid = c.stage_uid[stage_uid_base(c, b, batch_map_off(c, b, begin)) + k];
+        }
+        shade_one(c, sp, (int64_t)base.y + j, uid);
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -534,8 +667,8 @@ __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-    size_t map_off, counts, uid_off, round_off, stage_uid, stage_rn, stage_rp, flags, total;
-    int stage_factor;
+    size_t map_off, counts, tile_sums, tile_base, acc, stage_uid, stage_round, total;
+    int stage_factor, tile_batches, n_tiles;
 };
 
 static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr_batch_config* cfg) {
@@ -543,17 +676,20 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     const int ps = cfg->primitive_size, w = cfg->warp_width;
     L.stage_factor = 1;
     if (strategy == VR_WARP) L.stage_factor = (int)ceil_div(w, w - ps + 1 > 0 ? w - ps + 1 : 1);
+    // tiles: enough of them to fill 148 SMs several times over, at most kMaxTile batches each
+    int tb = 8;
+    while (tb < kMaxTile && nb / (2 * tb) >= 1184) tb <<= 1;
+    L.tile_batches = tb;
+    L.n_tiles = (int)ceil_div(nb > 0 ? nb : 1, tb);
     size_t o = 0;
     L.map_off = o; o += align_up((size_t)(nb + 1) * 4);
     L.counts = o; o += align_up((size_t)(nb + 1) * 8);
-    L.uid_off = o; o += align_up((size_t)(nb + 1) * 4);
-    L.round_off = o; o += align_up((size_t)(nb + 1) * 4);
-    L.flags = o; o += align_up(64);
+    L.tile_sums = o; o += align_up((size_t)(L.n_tiles + 1) * 8);
+    L.tile_base = o; o += align_up((size_t)(L.n_tiles + 1) * 8);
+    L.acc = o; o += align_up(ACC_WORDS * 8);
     L.stage_uid = o;
     if (strategy != VR_NAIVE) o += align_up(((size_t)span_total * L.stage_factor + (size_t)nb * ps + 64) * 4);
-    L.stage_rn = o;
-    if (strategy == VR_WARP) o += align_up(((size_t)span_total / ps + nb + 64) * 4);
-    L.stage_rp = o;
+    L.stage_round = o;
     if (strategy == VR_WARP) o += align_up(((size_t)span_total / ps + nb + 64) * 4);
     L.total = o;
     return L;
@@ -566,6 +702,15 @@ static cudaEvent_t g_prof_ev[VR_PROFILE_STAGES + 1];
 static int g_prof_on = 0, g_prof_marks = 0;
 static inline void prof_mark(cudaStream_t s) {
     if (g_prof_on && g_prof_marks <= VR_PROFILE_STAGES) cudaEventRecord(g_prof_ev[g_prof_marks++], s);
+}
+
+template <int W>
+static int launch_warp_tpb(const RunCtx& c, cudaStream_t stream) {
+    const size_t smem = (size_t)kTpbThreads * (2 * W * 6 + 16 * 4);
+    if (smem > 48 * 1024)
+        VR_CUDA_CHECK(cudaFuncSetAttribute(warp_tpb_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    warp_tpb_kernel<W><<<(int)ceil_div(c.n_batches, kTpbThreads), kTpbThreads, smem, stream>>>(c);
+    return VR_OK;
 }
 
 }  // namespace vr
@@ -664,6 +809,7 @@ int vr_static_offsets(int64_t n, const vr_batch_config* cfg, int32_t* d_offsets,
 int vr_output_bounds(int strategy, int64_t span_total, int64_t nb, const vr_batch_config* cfg,
                      const vr_hash_config* hcfg, int64_t* max_inv, int64_t* max_rounds) {
     (void)hcfg;
+    strategy &= 0xFF;
     if (strategy < VR_NAIVE || strategy > VR_PHASH) return VR_ERR_UNKNOWN_STRATEGY;
     int st = vr_check_batch_config(cfg);
     if (st) return st;
@@ -683,6 +829,7 @@ int vr_output_bounds(int strategy, int64_t span_total, int64_t nb, const vr_batc
 size_t vr_run_workspace_bytes(int strategy, int64_t span_total, int64_t nb, const vr_batch_config* cfg,
                               const vr_hash_config* hcfg) {
     (void)hcfg;
+    strategy &= 0xFF;
     if (vr_check_batch_config(cfg)) return 0;
     if (strategy == VR_WARP && cfg->warp_width < cfg->primitive_size) return 0;
     return ws_layout(strategy, span_total, nb, cfg).total;
@@ -692,6 +839,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
            int64_t nb, int64_t span_total, int32_t max_span, const vr_batch_config* cfg, const vr_hash_config* hcfg,
            const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_) {
     const bool no_budget = (strategy & VR_FLAG_NO_BUDGET) != 0;
+    const bool contiguous = (strategy & VR_FLAG_CONTIGUOUS) != 0;
     strategy &= 0xFF;
     if (strategy < VR_NAIVE || strategy > VR_PHASH) return VR_ERR_UNKNOWN_STRATEGY;  // strategies.py:422-423
     int st = vr_check_batch_config(cfg);
@@ -714,6 +862,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (max_span < ps) max_span = ps;
     WsLayout L = ws_layout(strategy, span_total, nb, cfg);
     if (ws_bytes < L.total || !d_ws) return VR_ERR_WORKSPACE;
+
     RunCtx c{};
     c.idx = d_idx; c.n_idx = n_idx; c.bbegin = d_bbegin; c.bend = d_bend;
     c.n_batches = (int)nb; c.max_span = max_span; c.ps = ps; c.max_unique = cfg->max_unique;
@@ -721,16 +870,18 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     c.table_bits = ilog2(hc.table_size);
     c.enforce_budget = strategy >= VR_SORT && !no_budget;
     c.stage_factor = L.stage_factor;
+    c.contiguous = contiguous ? 1 : 0;
+    c.tile_batches = L.tile_batches;
+    c.n_tiles = nb > 0 ? L.n_tiles : 0;
+    c.span_cap = span_total;
     unsigned char* ws = (unsigned char*)d_ws;
     c.map_off = (int32_t*)(ws + L.map_off);
     c.counts = (int2*)(ws + L.counts);
-    c.uid_off = (int32_t*)(ws + L.uid_off);
-    c.round_off = (int32_t*)(ws + L.round_off);
-    c.span_cap = span_total;
+    c.tile_sums = (int2*)(ws + L.tile_sums);
+    c.tile_base = (int2*)(ws + L.tile_base);
+    c.acc = (long long*)(ws + L.acc);
     c.stage_uid = (uint32_t*)(ws + L.stage_uid);
-    c.stage_rn = (int32_t*)(ws + L.stage_rn);
-    c.stage_rp = (int32_t*)(ws + L.stage_rp);
-    c.flags = (int32_t*)(ws + L.flags);
+    c.stage_round = (uint32_t*)(ws + L.stage_round);
     c.out = *out;
     ShaderParams sp{};
     if (shader) {
@@ -740,45 +891,57 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         sp.attr_words = shader->d_attributes ? shader->attr_words : 0; sp.vertex_count = shader->vertex_count;
         if (sp.kind == VR_SHADER_POSITION && (!sp.pos4 || !out->d_shaded4)) return VR_ERR_BAD_CONFIG;
     }
+    const int nbi = (int)nb;
+    // limits of the CTA-per-batch kernels
+    int pmax = 0, nmax = 0, q = 0;
+    size_t smem = 0;
+    if (strategy == VR_SORT && nb > 0) {
+        if (max_span > 8192) return VR_ERR_UNSUPPORTED;
+        pmax = (int)next_pow2((uint32_t)(max_span < 2 ? 2 : max_span));
+        smem = (size_t)pmax * (8 + 4 + 2);
+        VR_CUDA_CHECK(cudaFuncSetAttribute(sort_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    } else if (strategy == VR_HASH && nb > 0) {
+        nmax = (max_span + 3) & ~3;
+        q = (int)next_pow2((uint32_t)(2 * nmax < 64 ? 64 : 2 * nmax));
+        smem = (size_t)nmax * 4 + (size_t)q * 8 + (size_t)hc.table_size * 12 + (size_t)nmax * 2 + (size_t)nmax + 16;
+        if (smem > 200 * 1024 || max_span > 65535) return VR_ERR_UNSUPPORTED;
+        VR_CUDA_CHECK(cudaFuncSetAttribute(hash_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    }
 
     g_prof_marks = 0;
     prof_mark(stream);
-    span_scan_kernel<<<1, 1024, 0, stream>>>(c);
+    init_kernel<<<1, 32, 0, stream>>>(c);
+    if (!contiguous && nb > 0) span_scan_kernel<<<1, 1024, 0, stream>>>(c);
     prof_mark(stream);
     if (nb > 0) {
-        const int nbi = (int)nb;
         if (strategy == VR_NAIVE) {
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
         } else if (strategy == VR_WARP) {
-            warp_generic_kernel<<<(nbi + 127) / 128, 128, 0, stream>>>(c);
+            switch (cfg->warp_width) {
+            case 4: st = launch_warp_tpb<4>(c, stream); break;
+            case 8: st = launch_warp_tpb<8>(c, stream); break;
+            case 16: st = launch_warp_tpb<16>(c, stream); break;
+            case 32: st = launch_warp_tpb<32>(c, stream); break;
+            default: st = launch_warp_tpb<64>(c, stream); break;
+            }
+            if (st) return st;
         } else if (strategy == VR_SORT) {
-            if (max_span > 8192) return VR_ERR_UNSUPPORTED;
-            int pmax = (int)next_pow2((uint32_t)(max_span < 2 ? 2 : max_span));
-            size_t smem = (size_t)pmax * (8 + 4 + 2);
-            VR_CUDA_CHECK(cudaFuncSetAttribute(sort_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             sort_batch_kernel<<<nbi, 256, smem, stream>>>(c, pmax);
         } else {
-            int nmax = (max_span + 3) & ~3;
-            int q = (int)next_pow2((uint32_t)(2 * nmax < 64 ? 64 : 2 * nmax));
-            size_t smem = (size_t)nmax * 4 + (size_t)q * 8 + (size_t)hc.table_size * 12 + (size_t)nmax * 2 + (size_t)nmax + 16;
-            if (smem > 200 * 1024 || max_span > 65535) return VR_ERR_UNSUPPORTED;
-            VR_CUDA_CHECK(cudaFuncSetAttribute(hash_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             hash_batch_kernel<<<nbi, 256, smem, stream>>>(c, nmax, q);
         }
     }
     prof_mark(stream);
-    count_scan_kernel<<<1, 1024, 0, stream>>>(c);
+    if (nb > 0) tile_reduce_kernel<<<L.n_tiles, 128, 0, stream>>>(c);
+    tile_scan_kernel<<<1, 1024, 0, stream>>>(c);
     prof_mark(stream);
     if (nb > 0) {
-        const int blocks = (int)ceil_div(nb, 8);
         switch (strategy) {
-        case VR_NAIVE: finalize_kernel<VR_NAIVE><<<blocks, 256, 0, stream>>>(c, sp); break;
-        case VR_WARP: finalize_kernel<VR_WARP><<<blocks, 256, 0, stream>>>(c, sp); break;
-        default: finalize_kernel<VR_SORT><<<blocks, 256, 0, stream>>>(c, sp); break;
+        case VR_NAIVE: finalize_kernel<VR_NAIVE><<<L.n_tiles, kFinThreads, 0, stream>>>(c, sp); break;
+        case VR_WARP: finalize_kernel<VR_WARP><<<L.n_tiles, kFinThreads, 0, stream>>>(c, sp); break;
+        default: finalize_kernel<VR_SORT><<<L.n_tiles, kFinThreads, 0, stream>>>(c, sp); break;
         }
     }
-    prof_mark(stream);
-    finish_stats_kernel<<<1, 32, 0, stream>>>(c);
     prof_mark(stream);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;

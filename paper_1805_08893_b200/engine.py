@@ -252,13 +252,18 @@ class RunBuffers:
 def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_end: torch.Tensor,
                n_batches: int, span_total: int, max_span: int, cfg: BatchConfig, hcfg=None,
                shader: ShaderSpec | None = None, *, want_counts: bool = False,
-               buffers: RunBuffers | None = None, enforce_budget: bool = True) -> DeviceRun:
+               buffers: RunBuffers | None = None, enforce_budget: bool = True,
+               contiguous: bool | None = None) -> DeviceRun:
     """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back."""
     lib = N.require_cuda()
     if strategy not in N.STRATEGY_IDS:
         raise ConfigError(f"unknown strategy {strategy!r}; expected one of {tuple(N.STRATEGY_IDS)}")
     sid = N.STRATEGY_IDS[strategy]
     dev = d_indices.device
+    if contiguous is None:  # begin/end are two views of one offsets array
+        contiguous = (n_batches > 0 and d_begin.data_ptr() + 4 == d_end.data_ptr()
+                      and d_begin.is_contiguous() and d_end.is_contiguous())
+    flags = (0 if enforce_budget else N.VR_FLAG_NO_BUDGET) | (N.VR_FLAG_CONTIGUOUS if contiguous else 0)
     shader = shader or ShaderSpec()
     buffers = buffers or RunBuffers()
     c = _cfg_c(cfg)
@@ -305,7 +310,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         run.shade_counts.data_ptr() if run.shade_counts is not None else None,
         run.stats_dev.data_ptr(), max_inv.value, max_rounds.value)
     with torch.cuda.device(dev):
-        st = lib.vr_run(sid | (0 if enforce_budget else N.VR_FLAG_NO_BUDGET), _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
+        st = lib.vr_run(sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
                         span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws),
                         ws.numel(), _stream_ptr())
     raise_status(st)

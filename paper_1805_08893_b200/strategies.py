@@ -315,6 +315,7 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
         nb = max(int(batches.numel()) - 1, 0)
         max_span = max(cfg.batch_size, cfg.max_indices)
         span_total = n_idx
+        contiguous = True
     else:
         nb = len(batches)
         if nb:
@@ -326,6 +327,7 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
                 raise ConfigError(f"batch {batches[k]} is not a primitive-aligned range of the buffer")
             max_span = int((be - bb).max())
             span_total = int((be - bb).sum())
+            contiguous = bool((bb[1:] == be[:-1]).all())
 
     if strategy in ("hash", "phash"):
         hash_cfg = hash_cfg or HashConfig(table_size=cfg.block_size)  # strategies.py:431
@@ -355,7 +357,7 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
         d_begin, d_end = both[0], both[1]
     spec, positions = _shader_spec(shader, dev, vertex_count)
     run = engine.run_device(strategy, d_idx, d_begin, d_end, nb, span_total, max_span, cfg, hash_cfg,
-                            spec, want_counts=vertex_count is not None)
+                            spec, want_counts=vertex_count is not None, contiguous=contiguous)
     run.check()
 
     shade_counts = None
