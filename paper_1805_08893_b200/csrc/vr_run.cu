@@ -6,12 +6,13 @@
 //   K1 dedup_*       one thread / CTA per batch: validation (strategies.py:426-428) and the
 //                    strategy's dedup (strategies.py:159-298) -> assembly map (final), unique
 //                    ids and round records (staged), per-batch (rounds, invocations)
-//   K2 tile_reduce + tile_scan
-//                    two-level exclusive scan of (rounds, invocations) over tiles of batches
-//                    -> output offsets, totals, statistics (strategies.py:472-483)
-//   K3 finalize      one CTA per tile: round tables and unique ids to their final offsets and
-//                    the vertex shader once per unique id (strategies.py:456-463), 16-byte
-//                    gathers / coalesced 16-byte stores, optional per-vertex tally (:485-489)
+//   K2 scan          exclusive scan of (rounds, invocations) over SEGMENTS (a batch, or the 32
+//                    batches of one warp of the warp-voting kernel) -> output offsets,
+//                    totals, statistics (strategies.py:472-483)
+//   K3 shade         one warp per segment: round tables and unique ids to their final
+//                    offsets and the vertex shader once per unique id
+//                    (strategies.py:456-463), 16-byte gathers / coalesced 16-byte stores,
+//                    optional attribute pass-through and per-vertex tally (:485-489)
 #include "vr_common.cuh"
 
 namespace vr {
@@ -34,14 +35,17 @@ struct RunCtx {
     int enforce_budget;  // strategies.py:451-455 applies to sort/hash/phash
     int stage_factor;    // staged unique ids per batch <= span * stage_factor
     int contiguous;      // batches tile [bbegin[0], bend[n-1]) in order: map offset = begin - first
-    int tile_batches;    // batches per scan / finalize tile
-    int n_tiles;
+    int seg_batches;     // batches per segment: 32 for the warp-voting kernel, else 1
+    int n_segs;
+    int n_scan_tiles;    // 1024-segment tiles of the three-kernel scan (0: single-CTA scan)
     int64_t span_cap;    // caller's bound on the sum of batch spans
     // workspace
     int32_t* map_off;       // [n_batches+1] (non-contiguous lists only)
     int2* counts;           // [n_batches] (rounds, invocations)
-    int2* tile_sums;        // [n_tiles]
-    int2* tile_base;        // [n_tiles+1] exclusive prefix of tile_sums
+    int2* seg_counts;       // [n_segs] (aliases counts when seg_batches == 1)
+    int2* seg_off;          // [n_segs+1] exclusive prefix of seg_counts
+    int2* tile_sums;        // [n_scan_tiles] / tile_off [n_scan_tiles+1]
+    int2* tile_off;
     uint32_t* stage_uid;    // staged unique ids
     uint32_t* stage_round;  // staged round records: primitives << 8 | claims (warp)
     long long* acc;         // [ACC_WORDS]
@@ -60,7 +64,7 @@ __device__ __forceinline__ int batch_map_off(const RunCtx& c, int b, int begin) 
     return c.contiguous ? begin - __ldg(c.bbegin) : c.map_off[b];
 }
 __device__ __forceinline__ int64_t stage_uid_base(const RunCtx& c, int b, int mo) {
-    return (int64_t)mo * c.stage_factor + (int64_t)b * c.ps;
+    return ((int64_t)mo * c.stage_factor + (int64_t)b * 8) & ~3LL;  // 16-byte aligned, >= 5 words of slack
 }
 __device__ __forceinline__ int64_t stage_round_base(const RunCtx& c, int b, int mo) {
     return (int64_t)mo / c.ps + b;
@@ -149,46 +153,82 @@ __global__ void __launch_bounds__(256) naive_counts_kernel(RunCtx c) {
 // ---------------------------------------------------------------------------------
 constexpr int kTpbThreads = 128;
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) { uint32_t v; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) { uint16_t v; asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a)); return v; }
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) { uint32_t v; asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a)); return v; }
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) { asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((uint16_t)v) : "memory"); }
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+
+__device__ __forceinline__ uint4 lds_u128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+// 16-byte asynchronous global->shared copy (LDGSTS); bytes past src_bytes are zero-filled.
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int W>
 __global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
     constexpr int S = 2 * W;  // table slots per thread
+    constexpr int LOG2W = W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : W == 32 ? 5 : 6;
+    constexpr int LOG2S = LOG2W + 1;
+    constexpr uint32_t kRankMask = W - 1;
+    constexpr uint32_t kTagFree = (1u << (8 - LOG2W)) - 1;  // tag value of an unused entry (0xFF >> LOG2W)
+    constexpr int T = kTpbThreads;
+    // shared memory per thread: index quads uint4[4] (cp.async ring) | claims u32[W] |
+    // table u8[S] (tag << LOG2W | rank) | ring u16[16]; every array is [entry][thread], so a
+    // warp access with any per-lane entry is conflict-free for the 16-/4-byte arrays and at
+    // most 4-/2-way for the byte / half arrays.
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);                 // [S][T]
-    uint32_t* ring = keys + S * kTpbThreads;                                // [16][T]
-    uint16_t* tags = reinterpret_cast<uint16_t*>(ring + 16 * kTpbThreads);  // [S][T] tag<<6 | rank
-    const int t = threadIdx.x;
-    const int b = blockIdx.x * kTpbThreads + t;
+    int t = threadIdx.x;
+    asm volatile("" : "+r"(t));  // keep the thread id in a register (no S2R per use)
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t a_quads = sbase + 16 * t;                                  // + 16*T*(quad & 3)
+    const uint32_t a_claims = sbase + 64 * T + 4 * t;                         // + 4*T*rank
+    // byte / half arrays keep each thread's entries inside its own 32-bit column:
+    //   table slot h  -> word (h >> 2) of the column, byte h & 3
+    //   ring  pos  p  -> word ((p >> 1) & 7) of the column, half p & 1
+    const uint32_t a_table = sbase + 64 * T + 4 * T * W + 4 * t;
+    const uint32_t a_ring = sbase + 64 * T + 4 * T * W + T * S + 4 * t;
+    auto tab = [&](uint32_t h) { return a_table + 4 * T * (h >> 2) + (h & 3); };
+    auto rng = [&](int p) { return a_ring + 4 * T * ((p >> 1) & 7) + 2 * (p & 1); };
+    const int b = blockIdx.x * T + t;
 #pragma unroll
-    for (int h = 0; h < S; h++) tags[h * kTpbThreads + t] = 0xFFFFu;
-    if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
-    int begin, n;
-    if (!validate_batch(c, b, begin, n)) { c.counts[b] = make_int2(0, 0); return; }
-    const int mo = batch_map_off(c, b, begin);
+    for (int h = 0; h < S / 4; h++) sts_u32(a_table + 4 * T * h, 0xFFFFFFFFu);
+    bool active = b < c.n_batches && !c.acc[ACC_ABORT];
+    int begin = 0, n = 0;
+    if (active && !validate_batch(c, b, begin, n)) { c.counts[b] = make_int2(0, 0); active = false; }
+    const int mo = active ? batch_map_off(c, b, begin) : 0;
     const int ps = c.ps;
-    uint16_t* __restrict__ amap = c.out.d_assembly_map ? c.out.d_assembly_map + mo : nullptr;
+    uint16_t* __restrict__ amap = (active && c.out.d_assembly_map) ? c.out.d_assembly_map + mo : nullptr;
     const bool amap_vec = (mo & 7) == 0;
     uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
     uint32_t* __restrict__ srd = c.stage_round + stage_round_base(c, b, mo);
-    const uint4* __restrict__ quads = reinterpret_cast<const uint4*>(c.idx);
-    const int64_t n_quads_full = c.n_idx >> 2;  // quads that lie completely inside the buffer
+    const int n_idx = (int)c.n_idx;
 
-    auto load_quad = [&](int64_t gq) -> uint4 {
-        if (gq < n_quads_full) return __ldg(quads + gq);
-        uint4 v = make_uint4(0, 0, 0, 0);
-        const int64_t g = gq << 2;
-        if (g + 0 < c.n_idx) v.x = __ldg(c.idx + g + 0);
-        if (g + 1 < c.n_idx) v.y = __ldg(c.idx + g + 1);
-        if (g + 2 < c.n_idx) v.z = __ldg(c.idx + g + 2);
-        return v;
+    // index stream: quad q of the buffer lives in ring slot q & 3; quads up to (current + 2)
+    // are in flight, the previous quad is still resident for the <= 2-slot rewind of a round end
+    auto issue_quad = [&](int gq) {
+        const int rem = n_idx - 4 * gq;  // indices left from this quad on
+        const int bytes = rem >= 4 ? 16 : (rem > 0 ? 4 * rem : 0);
+        cp_async16(a_quads + 16 * T * (gq & 3), c.idx + (bytes ? 4 * (int64_t)gq : 0), bytes);
+        cp_async_commit();
     };
-    int64_t cq = ((int64_t)begin) >> 2;
-    uint4 cur = load_quad(cq), nxt = load_quad(cq + 1);
-
     auto flush_group = [&](int g, int count) {
         if (!amap) return;
         uint32_t r[8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) r[j] = ring[((8 * g + j) & 15) * kTpbThreads + t];
+        for (int j = 0; j < 4; j++) {  // two ranks per 32-bit word of the ring
+            const uint32_t w2 = lds_u32(a_ring + 4 * T * ((4 * g + j) & 7));
+            r[2 * j] = w2 & 0xFFFFu;
+            r[2 * j + 1] = w2 >> 16;
+        }
         if (count == 8 && amap_vec) {
             uint4 v = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), r[4] | (r[5] << 16), r[6] | (r[7] << 16));
             *reinterpret_cast<uint4*>(amap + 8 * g) = v;
@@ -199,61 +239,100 @@ __global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
         }
     };
 
-    int cursor = 0, rounds = 0, inv = 0, flushed = 0;
+    int issued = (begin >> 2) - 1;  // highest quad handed to cp.async
+    if (active) { issue_quad(++issued); issue_quad(++issued); }
+    int cursor = 0, i = 0, fill = 0, stop = n, rounds = 0, inv = 0, flushed = 0, done = 0;
     uint32_t tagno = 0;
-    bool failed = false;
-    while (cursor < n) {
-        int fill = 0, stop = n, done;
-        int i = cursor;
+    bool run = false, round_end = false, finished = false;
+    uint4 cl = make_uint4(0, 0, 0, 0);  // up to four staged claims not yet written
+
+    // One index slot of this lane's batch (strategies.py:204-213 for one lane of the fetch).
+    auto element = [&](const int e, const uint32_t x) {
+        if (!run || ((begin + i) & 3) != e) return;
+        if (i >= stop) { done = stop; round_end = true; run = false; return; }
+        uint32_t h = (x * 0x9E3779B1u) >> (32 - LOG2S);
+        int r = -1;
         for (;;) {
-            if (i >= stop) { done = stop; break; }
-            const int64_t g = (int64_t)begin + i;
-            const int64_t gq = g >> 2;
-            if (gq != cq) {
-                cur = (gq == cq + 1) ? nxt : load_quad(gq);
-                cq = gq;
-                nxt = load_quad(gq + 1);
-            }
-            const int lane4 = (int)(g & 3);
-            const uint32_t x = lane4 == 0 ? cur.x : lane4 == 1 ? cur.y : lane4 == 2 ? cur.z : cur.w;
-            uint32_t h = (x ^ (x >> 7) ^ (x >> 13)) & (S - 1);
-            int r = -1;
-            for (;;) {
-                const uint32_t tg = tags[h * kTpbThreads + t];
-                if ((tg >> 6) != tagno) break;  // free: never used or left over from an earlier round
-                if (keys[h * kTpbThreads + t] == x) { r = (int)(tg & 63u); break; }
-                h = (h + 1) & (S - 1);
-            }
-            if (r < 0) {
-                if (fill >= W) { done = i; break; }  // first unassignable slot
-                keys[h * kTpbThreads + t] = x;
-                tags[h * kTpbThreads + t] = (uint16_t)((tagno << 6) | (uint32_t)fill);
-                suid[inv + fill] = x;
-                r = fill++;
-                if (fill == W) stop = min(n, cursor + ((i - cursor) / W + 1) * W);
-            }
-            ring[(i & 15) * kTpbThreads + t] = (uint32_t)r;
-            if (i >= 8 * flushed + 10) { flush_group(flushed, 8); flushed++; }  // positions <= i-3 are final
-            i++;
+            const uint32_t ent = lds_u8(tab(h));
+            if ((ent >> LOG2W) != tagno) break;  // free: never used or left over from an earlier round
+            const uint32_t rr = ent & kRankMask;
+            if (lds_u32(a_claims + 4 * T * rr) == x) { r = (int)rr; break; }
+            h = (h + 1) & (S - 1);
         }
-        const int emitted = (done - cursor) / ps;
-        if (emitted == 0) {  // strategies.py:226-227 (unreachable for W >= ps)
-            report_error(c, b, VR_ERR_WARP_NO_PROGRESS);
-            failed = true;
-            break;
+        if (r < 0) {
+            if (fill >= W) { done = i; round_end = true; run = false; return; }  // first unassignable slot
+            sts_u32(a_claims + 4 * T * fill, x);
+            sts_u8(tab(h), (tagno << LOG2W) | (uint32_t)fill);
+            {   // staged claims leave as 16-byte stores (the staging base is 16-byte aligned)
+                const int k = inv + fill;
+                const int k4 = k & 3;
+                if (k4 == 0) cl.x = x; else if (k4 == 1) cl.y = x; else if (k4 == 2) cl.z = x; else cl.w = x;
+                if (k4 == 3) *reinterpret_cast<uint4*>(suid + (k & ~3)) = cl;
+            }
+            r = fill++;
+            if (fill == W) stop = min(n, cursor + ((i - cursor) / W + 1) * W);
         }
-        srd[rounds] = ((uint32_t)emitted << 8) | (uint32_t)fill;
-        rounds++;
-        inv += fill;
-        cursor += emitted * ps;
-        if (++tagno == 1023u) {  // tag space exhausted: wipe this thread's column
-            for (int h = 0; h < S; h++) tags[h * kTpbThreads + t] = 0xFFFFu;
-            tagno = 0;
+        sts_u16(rng(i), (uint32_t)r);
+        i++;
+    };
+
+    // One loop for the whole warp, re-converged every iteration: each lane advances its own
+    // batch by up to one 16-byte quad of indices; round ends and batch ends are handled in place.
+    while (__any_sync(0xffffffffu, active)) {
+        if (!active) continue;
+        const int gq = (begin + i) >> 2;
+        if (issued < gq + 2) issue_quad(++issued);  // one new quad per forward step
+        else cp_async_commit();                     // keep one group per iteration
+        cp_async_wait<2>();                         // everything but the two newest groups has landed
+        const uint4 q = lds_u128(a_quads + 16 * T * (gq & 3));
+        run = true;
+        round_end = false;
+        element(0, q.x);
+        element(1, q.y);
+        element(2, q.z);
+        element(3, q.w);
+        if (i >= 8 * flushed + 10) {  // positions <= i-3 are final
+            flush_group(flushed, 8);
+            flushed++;
+        }
+        if (round_end) {
+            const int emitted = (done - cursor) / ps;
+            if (emitted == 0) {  // strategies.py:226-227 (unreachable for W >= ps)
+                report_error(c, b, VR_ERR_WARP_NO_PROGRESS);
+                c.counts[b] = make_int2(0, 0);
+                active = false;
+                continue;
+            }
+            srd[rounds] = ((uint32_t)emitted << 8) | (uint32_t)fill;
+            rounds++;
+            inv += fill;
+            cursor += emitted * ps;
+            i = cursor;
+            fill = 0;
+            stop = n;
+            if (++tagno == kTagFree) {  // tag space exhausted: wipe this thread's column
+                for (int h = 0; h < S / 4; h++) sts_u32(a_table + 4 * T * h, 0xFFFFFFFFu);
+                tagno = 0;
+            }
+            if (cursor >= n) {
+                for (int g = flushed; 8 * g < n; g++) flush_group(g, min(8, n - 8 * g));
+                if (inv & 3) *reinterpret_cast<uint4*>(suid + (inv & ~3)) = cl;  // partial last group
+                c.counts[b] = make_int2(rounds, inv);
+                finished = true;
+                active = false;
+            }
         }
     }
-    if (failed) { c.counts[b] = make_int2(0, 0); return; }
-    for (int g = flushed; 8 * g < n; g++) flush_group(g, min(8, n - 8 * g));
-    c.counts[b] = make_int2(rounds, inv);
+    cp_async_wait<0>();
+    // the 32 batches of this warp form one segment of the offset scan
+    int seg_r = finished ? rounds : 0, seg_u = finished ? inv : 0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        seg_r += __shfl_xor_sync(0xffffffffu, seg_r, d);
+        seg_u += __shfl_xor_sync(0xffffffffu, seg_u, d);
+    }
+    const int seg = b >> 5;
+    if ((t & 31) == 0 && seg < c.n_segs) c.seg_counts[seg] = make_int2(seg_r, seg_u);
 }
 
 // ---------------------------------------------------------------------------------
@@ -442,25 +521,37 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
 }
 
 // ---------------------------------------------------------------------------------
-// K2: two-level exclusive scan of per-batch (rounds, invocations).
+// K2: exclusive scan of per-segment (rounds, invocations).  Up to 32768 segments one CTA
+// does it all; beyond that, 1024-segment tiles are reduced, the tile sums scanned by the
+// same single-CTA kernel, and a down-sweep writes the per-segment offsets.
 // ---------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) tile_reduce_kernel(RunCtx c) {
-    __shared__ int sr[4], su[4];
-    const int tile = blockIdx.x, tid = threadIdx.x;
-    const int b0 = tile * c.tile_batches, b1 = min(c.n_batches, b0 + c.tile_batches);
-    int r = 0, u = 0;
-    for (int b = b0 + tid; b < b1; b += 128) { int2 v = c.counts[b]; r += v.x; u += v.y; }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        r += __shfl_xor_sync(0xffffffffu, r, d);
-        u += __shfl_xor_sync(0xffffffffu, u, d);
+__device__ void finish_stats(const RunCtx& c, long long R, long long U) {
+    int64_t* st = c.out.d_stats;
+    for (int i = 0; i < VR_STATS_WORDS; i++) st[i] = 0;
+    long long span_total = 0;
+    if (c.n_batches > 0)
+        span_total = c.contiguous ? (long long)c.bend[c.n_batches - 1] - c.bbegin[0] : c.map_off[c.n_batches];
+    if (span_total > c.span_cap) report_error(c, 0, VR_ERR_CAPACITY);
+    if (U > c.out.cap_unique || R > c.out.cap_rounds || U > 0x7fffffffLL) report_error(c, 0, VR_ERR_CAPACITY);
+    st[VR_STAT_INDICES] = span_total;
+    st[VR_STAT_INVOCATIONS] = U;
+    st[VR_STAT_BATCHES] = c.n_batches;
+    st[VR_STAT_ROUNDS] = R;
+    st[VR_STAT_PROBES_FAST] = c.acc[ACC_PROBES_FAST];
+    st[VR_STAT_PROBES_SLOW] = c.acc[ACC_PROBES_SLOW];
+    st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
+    const long long e = c.acc[ACC_ERROR];
+    if (e == 0) {
+        st[VR_STAT_ERROR] = -1;
+        if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
+        if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
+    } else {
+        st[VR_STAT_ERROR] = ((0x7FFFFFFFFFFFLL - (e >> 8)) << 8) | (e & 0xFF);
+        c.acc[ACC_ABORT] = 1;  // K3 must not touch the outputs
     }
-    if ((tid & 31) == 0) { sr[tid >> 5] = r; su[tid >> 5] = u; }
-    __syncthreads();
-    if (tid == 0) c.tile_sums[tile] = make_int2(sr[0] + sr[1] + sr[2] + sr[3], su[0] + su[1] + su[2] + su[3]);
 }
 
-__global__ void __launch_bounds__(1024) tile_scan_kernel(RunCtx c) {
+__global__ void __launch_bounds__(1024) scan_block_kernel(RunCtx c, const int2* __restrict__ in, int2* __restrict__ out, int n) {
     __shared__ int scratch[40];
     __shared__ int chunk_r[1024];
     __shared__ int chunk_u[1024];
@@ -468,139 +559,169 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(RunCtx c) {
     const int tid = threadIdx.x;
     if (tid == 0) { carry_r = 0; carry_u = 0; }
     __syncthreads();
-    for (int base = 0; base < c.n_tiles; base += 1024) {
+    for (int base = 0; base < n; base += 1024) {
         int k = base + tid;
-        int2 v = k < c.n_tiles ? c.tile_sums[k] : make_int2(0, 0);
+        int2 v = k < n ? in[k] : make_int2(0, 0);
         chunk_r[tid] = v.x;
         chunk_u[tid] = v.y;
         __syncthreads();
         int tr = block_exclusive_scan(chunk_r, 1024, scratch);
         int tu = block_exclusive_scan(chunk_u, 1024, scratch);
         long long br = carry_r, bu = carry_u;
-        if (k < c.n_tiles)
-            c.tile_base[k] = make_int2((int)min(br + chunk_r[tid], 0x7fffffffLL), (int)min(bu + chunk_u[tid], 0x7fffffffLL));
+        if (k < n) out[k] = make_int2((int)min(br + chunk_r[tid], 0x7fffffffLL), (int)min(bu + chunk_u[tid], 0x7fffffffLL));
         __syncthreads();
         if (tid == 0) { carry_r = br + tr; carry_u = bu + tu; }
         __syncthreads();
     }
     if (tid == 0) {
-        const long long R = carry_r, U = carry_u;
-        c.tile_base[c.n_tiles] = make_int2((int)min(R, 0x7fffffffLL), (int)min(U, 0x7fffffffLL));
-        int64_t* st = c.out.d_stats;
-        for (int i = 0; i < VR_STATS_WORDS; i++) st[i] = 0;
-        long long span_total = 0;
-        if (c.n_batches > 0)
-            span_total = c.contiguous ? (long long)c.bend[c.n_batches - 1] - c.bbegin[0] : c.map_off[c.n_batches];
-        if (span_total > c.span_cap) report_error(c, 0, VR_ERR_CAPACITY);
-        if (U > c.out.cap_unique || R > c.out.cap_rounds || U > 0x7fffffffLL) report_error(c, 0, VR_ERR_CAPACITY);
-        st[VR_STAT_INDICES] = span_total;
-        st[VR_STAT_INVOCATIONS] = U;
-        st[VR_STAT_BATCHES] = c.n_batches;
-        st[VR_STAT_ROUNDS] = R;
-        st[VR_STAT_PROBES_FAST] = c.acc[ACC_PROBES_FAST];
-        st[VR_STAT_PROBES_SLOW] = c.acc[ACC_PROBES_SLOW];
-        st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
-        const long long e = c.acc[ACC_ERROR];
-        if (e == 0) {
-            st[VR_STAT_ERROR] = -1;
-            if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
-            if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
-        } else {
-            st[VR_STAT_ERROR] = ((0x7FFFFFFFFFFFLL - (e >> 8)) << 8) | (e & 0xFF);
-            c.acc[ACC_ABORT] = 1;  // K3 must not touch the outputs
+        out[n] = make_int2((int)min((long long)carry_r, 0x7fffffffLL), (int)min((long long)carry_u, 0x7fffffffLL));
+        finish_stats(c, carry_r, carry_u);
+    }
+}
+
+__global__ void __launch_bounds__(256) scan_reduce_kernel(RunCtx c) {
+    __shared__ int sr[8], su[8];
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int k0 = tile * 1024, k1 = min(c.n_segs, k0 + 1024);
+    int r = 0, u = 0;
+    for (int k = k0 + tid; k < k1; k += 256) { int2 v = c.seg_counts[k]; r += v.x; u += v.y; }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        r += __shfl_xor_sync(0xffffffffu, r, d);
+        u += __shfl_xor_sync(0xffffffffu, u, d);
+    }
+    if ((tid & 31) == 0) { sr[tid >> 5] = r; su[tid >> 5] = u; }
+    __syncthreads();
+    if (tid == 0) {
+        int tr = 0, tu = 0;
+        for (int w = 0; w < 8; w++) { tr += sr[w]; tu += su[w]; }
+        c.tile_sums[tile] = make_int2(tr, tu);
+    }
+}
+
+__global__ void __launch_bounds__(1024) scan_down_kernel(RunCtx c) {
+    __shared__ int scratch[40];
+    __shared__ int chunk_r[1024];
+    __shared__ int chunk_u[1024];
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int k = tile * 1024 + tid;
+    int2 v = k < c.n_segs ? c.seg_counts[k] : make_int2(0, 0);
+    chunk_r[tid] = v.x;
+    chunk_u[tid] = v.y;
+    __syncthreads();
+    block_exclusive_scan(chunk_r, 1024, scratch);
+    block_exclusive_scan(chunk_u, 1024, scratch);
+    const int2 base = c.tile_off[tile];
+    if (k < c.n_segs) c.seg_off[k] = make_int2(base.x + chunk_r[tid], base.y + chunk_u[tid]);
+    if (k == c.n_segs - 1) c.seg_off[c.n_segs] = c.tile_off[c.n_scan_tiles];
+}
+
+// ---------------------------------------------------------------------------------
+// K3: one warp per segment.
+// ---------------------------------------------------------------------------------
+constexpr int kShadeThreads = 256;
+constexpr int kShadeUnroll = 4;
+
+// Streams `cnt` staged unique ids src[0..cnt) to outputs dst0.. with `width` cooperating lanes
+// (l = lane within the group): coalesced id load, 16-byte gather, transform, coalesced stores.
+template <int STRATEGY>
+__device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams& sp, const uint32_t* __restrict__ src,
+                                             int cnt, int64_t dst0, int l, int width, int naive_mo) {
+    const bool want_uid = c.out.d_unique_ids != nullptr;
+    const bool want_pos = sp.kind == VR_SHADER_POSITION;
+    const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
+    const bool want_cnt = c.out.d_shade_counts != nullptr;
+    uint32_t* __restrict__ out_uid = c.out.d_unique_ids + dst0;
+    float4* __restrict__ shaded = reinterpret_cast<float4*>(c.out.d_shaded4) + dst0;
+    for (int j0 = 0; j0 < cnt; j0 += width * kShadeUnroll) {
+        uint32_t uid[kShadeUnroll];
+        float4 p[kShadeUnroll];
+#pragma unroll
+        for (int u = 0; u < kShadeUnroll; u++) {
+            const int j = j0 + u * width + l;
+            uid[u] = j < cnt ? src[j] : 0u;
+        }
+        if (want_pos) {
+#pragma unroll
+            for (int u = 0; u < kShadeUnroll; u++) {
+                const int j = j0 + u * width + l;
+                if (j < cnt) p[u] = __ldg(sp.pos4 + uid[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kShadeUnroll; u++) {
+            const int j = j0 + u * width + l;
+            if (j >= cnt) continue;
+            if (want_uid) out_uid[j] = uid[u];
+            if (want_pos) shaded[j] = transform_position(sp, p[u]);
+            if (STRATEGY == VR_NAIVE && c.out.d_assembly_map) c.out.d_assembly_map[naive_mo + j] = (uint16_t)(j % c.ps);
+            if (want_attr)
+                for (int k = 0; k < sp.attr_words; k++)
+                    c.out.d_shaded_attr[(dst0 + j) * sp.attr_words + k] = __ldg(sp.attr + (int64_t)uid[u] * sp.attr_words + k);
+            if (want_cnt) atomicAdd(&c.out.d_shade_counts[uid[u]], 1);
         }
     }
 }
 
-// ---------------------------------------------------------------------------------
-// K3: one CTA per tile of batches.
-// ---------------------------------------------------------------------------------
-__device__ __forceinline__ void shade_one(const RunCtx& c, const ShaderParams& sp, int64_t dst, uint32_t uid) {
-    if (c.out.d_unique_ids) c.out.d_unique_ids[dst] = uid;
-    if (sp.kind == VR_SHADER_POSITION)
-        reinterpret_cast<float4*>(c.out.d_shaded4)[dst] = shade_position(sp, uid);
-    if (sp.attr_words && c.out.d_shaded_attr)
-        for (int k = 0; k < sp.attr_words; k++)
-            c.out.d_shaded_attr[dst * sp.attr_words + k] = __ldg(sp.attr + (int64_t)uid * sp.attr_words + k);
-    if (c.out.d_shade_counts) atomicAdd(&c.out.d_shade_counts[uid], 1);
-}
-
-constexpr int kFinThreads = 256;
-constexpr int kMaxTile = 1024;
-
 template <int STRATEGY>
-__global__ void __launch_bounds__(kFinThreads) finalize_kernel(RunCtx c, ShaderParams sp) {
-    __shared__ int scratch[40];
-    __shared__ int uoff[kMaxTile + 1];  // tile-local exclusive offsets of unique ids
-    __shared__ int roff[kMaxTile + 1];  // tile-local exclusive offsets of rounds
-    if (c.acc[ACC_ABORT]) return;
-    const int tid = threadIdx.x;
-    const int tile = blockIdx.x;
-    const int b0 = tile * c.tile_batches;
-    const int nb = min(c.n_batches, b0 + c.tile_batches) - b0;
-    for (int i = tid; i < nb; i += kFinThreads) {
-        int2 v = c.counts[b0 + i];
-        roff[i] = v.x;
-        uoff[i] = v.y;
-    }
-    __syncthreads();
-    const int tile_rounds = block_exclusive_scan(roff, nb, scratch);
-    const int tile_inv = block_exclusive_scan(uoff, nb, scratch);
-    if (tid == 0) { roff[nb] = tile_rounds; uoff[nb] = tile_inv; }
-    __syncthreads();
-    const int2 base = c.tile_base[tile];
+__global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderParams sp) {
+    const int lane = threadIdx.x & 31;
+    const int s = blockIdx.x * (kShadeThreads / 32) + (threadIdx.x >> 5);
+    if (s >= c.n_segs || c.acc[ACC_ABORT]) return;
+    const int2 off = c.seg_off[s];
     const int ps = c.ps;
-    // round tables
-    for (int i = tid; i < nb; i += kFinThreads) {
-        const int b = b0 + i;
-        const int r0 = base.x + roff[i], u0 = base.y + uoff[i];
-        if (c.out.d_batch_round_off) c.out.d_batch_round_off[b] = r0;
-        if (STRATEGY == VR_WARP) {
-            const int begin = __ldg(c.bbegin + b);
-            const int mo = batch_map_off(c, b, begin);
-            const uint32_t* srd = c.stage_round + stage_round_base(c, b, mo);
-            const int nr = roff[i + 1] - roff[i];
+    if (STRATEGY == VR_WARP) {
+        // lanes <-> the 32 batches of the segment: round tables
+        const int b = 32 * s + lane;
+        const bool valid = b < c.n_batches;
+        const int2 cnt = valid ? c.counts[b] : make_int2(0, 0);
+        const int inc_r = warp_incl_scan(cnt.x, lane), inc_u = warp_incl_scan(cnt.y, lane);
+        const int begin = valid ? __ldg(c.bbegin + b) : 0;
+        const int mo = valid ? batch_map_off(c, b, begin) : 0;
+        const int u0 = off.y + inc_u - cnt.y;
+        if (valid) {
+            const int r0 = off.x + inc_r - cnt.x;
             int run = u0;
-            for (int r = 0; r < nr; r++) {
+            if (c.out.d_batch_round_off) c.out.d_batch_round_off[b] = r0;
+            const uint32_t* srd = c.stage_round + stage_round_base(c, b, mo);
+            for (int r = 0; r < cnt.x; r++) {
                 const uint32_t w = srd[r];
                 if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0 + r] = run;
                 if (c.out.d_round_prims) c.out.d_round_prims[r0 + r] = (int)(w >> 8);
                 run += (int)(w & 0xFFu);
             }
-        } else if (STRATEGY != VR_NAIVE) {
-            if (roff[i + 1] > roff[i]) {
-                const int span = __ldg(c.bend + b) - __ldg(c.bbegin + b);
-                if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0] = u0;
-                if (c.out.d_round_prims) c.out.d_round_prims[r0] = span / ps;
-            }
         }
-    }
-    if (STRATEGY == VR_NAIVE) {  // one round per primitive: closed form over the tile's rounds
-        for (int r = tid; r < tile_rounds; r += kFinThreads) {
-            if (c.out.d_round_uid_off) c.out.d_round_uid_off[base.x + r] = base.y + r * ps;
-            if (c.out.d_round_prims) c.out.d_round_prims[base.x + r] = 1;
+        // unique ids: each half-warp streams one batch at a time (a batch holds ~W ids)
+        const unsigned long long my_src = (unsigned long long)(c.stage_uid + stage_uid_base(c, b, mo));
+        const int half = lane >> 4, l = lane & 15;
+        for (int pair = 0; pair < 16; pair++) {
+            const int L = 2 * pair + half;
+            const int n_b = __shfl_sync(0xffffffffu, cnt.y, L);
+            const int d_b = __shfl_sync(0xffffffffu, u0, L);
+            const uint32_t* src = (const uint32_t*)__shfl_sync(0xffffffffu, my_src, L);
+            shade_stream<STRATEGY>(c, sp, src, n_b, d_b, l, 16, 0);
         }
-    }
-    // unique ids + shading: flat over the tile's outputs, batch found by bisection in smem
-    int steps = 0;
-    while ((1 << steps) < nb) steps++;
-    for (int j = tid; j < tile_inv; j += kFinThreads) {
-        int lo = 0;  // largest i with uoff[i] <= j
-        for (int s = steps - 1; s >= 0; s--) {
-            const int mid = lo + (1 << s);
-            if (mid < nb && uoff[mid] <= j) lo = mid;
-        }
-        const int b = b0 + lo;
-        const int k = j - uoff[lo];
+    } else {
+        const int b = s;
+        const int2 cnt = c.counts[b];
         const int begin = __ldg(c.bbegin + b);
-        uint32_t uid;
-        if (STRATEGY == VR_NAIVE) {
-            uid = __ldg(c.idx + begin + k);
-            if (c.out.d_assembly_map) c.out.d_assembly_map[batch_map_off(c, b, begin) + k] = (uint16_t)(k % ps);
+        const int mo = batch_map_off(c, b, begin);
+        if (lane == 0 && c.out.d_batch_round_off) c.out.d_batch_round_off[b] = off.x;
+        const uint32_t* src;
+        if (STRATEGY == VR_NAIVE) {  // one round per primitive, closed form
+            for (int r = lane; r < cnt.x; r += 32) {
+                if (c.out.d_round_uid_off) c.out.d_round_uid_off[off.x + r] = off.y + r * ps;
+                if (c.out.d_round_prims) c.out.d_round_prims[off.x + r] = 1;
+            }
+            src = c.idx + begin;
         } else {
-            uid = c.stage_uid[stage_uid_base(c, b, batch_map_off(c, b, begin)) + k];
+            if (lane == 0 && cnt.x > 0) {
+                if (c.out.d_round_uid_off) c.out.d_round_uid_off[off.x] = off.y;
+                if (c.out.d_round_prims) c.out.d_round_prims[off.x] = (__ldg(c.bend + b) - begin) / ps;
+            }
+            src = c.stage_uid + stage_uid_base(c, b, mo);
         }
-        shade_one(c, sp, (int64_t)base.y + j, uid);
+        shade_stream<STRATEGY>(c, sp, src, cnt.y, off.y, lane, 32, mo);
     }
 }
 
@@ -667,8 +788,8 @@ __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-    size_t map_off, counts, tile_sums, tile_base, acc, stage_uid, stage_round, total;
-    int stage_factor, tile_batches, n_tiles;
+    size_t map_off, counts, seg_counts, seg_off, tile_sums, tile_off, acc, stage_uid, stage_round, total;
+    int stage_factor, seg_batches, n_segs, n_scan_tiles;
 };
 
 static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr_batch_config* cfg) {
@@ -676,19 +797,20 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     const int ps = cfg->primitive_size, w = cfg->warp_width;
     L.stage_factor = 1;
     if (strategy == VR_WARP) L.stage_factor = (int)ceil_div(w, w - ps + 1 > 0 ? w - ps + 1 : 1);
-    // tiles: enough of them to fill 148 SMs several times over, at most kMaxTile batches each
-    int tb = 8;
-    while (tb < kMaxTile && nb / (2 * tb) >= 1184) tb <<= 1;
-    L.tile_batches = tb;
-    L.n_tiles = (int)ceil_div(nb > 0 ? nb : 1, tb);
+    L.seg_batches = strategy == VR_WARP ? 32 : 1;
+    L.n_segs = (int)ceil_div(nb, L.seg_batches);
+    L.n_scan_tiles = L.n_segs > 32768 ? (int)ceil_div(L.n_segs, 1024) : 0;
     size_t o = 0;
     L.map_off = o; o += align_up((size_t)(nb + 1) * 4);
     L.counts = o; o += align_up((size_t)(nb + 1) * 8);
-    L.tile_sums = o; o += align_up((size_t)(L.n_tiles + 1) * 8);
-    L.tile_base = o; o += align_up((size_t)(L.n_tiles + 1) * 8);
+    L.seg_counts = L.counts;
+    if (L.seg_batches > 1) { L.seg_counts = o; o += align_up((size_t)(L.n_segs + 1) * 8); }
+    L.seg_off = o; o += align_up((size_t)(L.n_segs + 2) * 8);
+    L.tile_sums = o; o += align_up((size_t)(L.n_scan_tiles + 1) * 8);
+    L.tile_off = o; o += align_up((size_t)(L.n_scan_tiles + 2) * 8);
     L.acc = o; o += align_up(ACC_WORDS * 8);
     L.stage_uid = o;
-    if (strategy != VR_NAIVE) o += align_up(((size_t)span_total * L.stage_factor + (size_t)nb * ps + 64) * 4);
+    if (strategy != VR_NAIVE) o += align_up(((size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64) * 4);
     L.stage_round = o;
     if (strategy == VR_WARP) o += align_up(((size_t)span_total / ps + nb + 64) * 4);
     L.total = o;
@@ -706,7 +828,7 @@ static inline void prof_mark(cudaStream_t s) {
 
 template <int W>
 static int launch_warp_tpb(const RunCtx& c, cudaStream_t stream) {
-    const size_t smem = (size_t)kTpbThreads * (2 * W * 6 + 16 * 4);
+    const size_t smem = (size_t)kTpbThreads * (64 + 4 * W + 2 * W + 2 * 16);
     if (smem > 48 * 1024)
         VR_CUDA_CHECK(cudaFuncSetAttribute(warp_tpb_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     warp_tpb_kernel<W><<<(int)ceil_div(c.n_batches, kTpbThreads), kTpbThreads, smem, stream>>>(c);
@@ -857,6 +979,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         return VR_ERR_UNSUPPORTED;
     if (strategy == VR_WARP && nb > 0 && cfg->warp_width < cfg->primitive_size) return VR_ERR_WARP_WIDTH;
     if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (((uintptr_t)d_idx & 15) != 0) return VR_ERR_UNSUPPORTED;  // 16-byte index loads
     cudaStream_t stream = (cudaStream_t)stream_;
     const int ps = cfg->primitive_size;
     if (max_span < ps) max_span = ps;
@@ -871,14 +994,17 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     c.enforce_budget = strategy >= VR_SORT && !no_budget;
     c.stage_factor = L.stage_factor;
     c.contiguous = contiguous ? 1 : 0;
-    c.tile_batches = L.tile_batches;
-    c.n_tiles = nb > 0 ? L.n_tiles : 0;
+    c.seg_batches = L.seg_batches;
+    c.n_segs = L.n_segs;
+    c.n_scan_tiles = L.n_scan_tiles;
     c.span_cap = span_total;
     unsigned char* ws = (unsigned char*)d_ws;
     c.map_off = (int32_t*)(ws + L.map_off);
     c.counts = (int2*)(ws + L.counts);
+    c.seg_counts = (int2*)(ws + L.seg_counts);
+    c.seg_off = (int2*)(ws + L.seg_off);
     c.tile_sums = (int2*)(ws + L.tile_sums);
-    c.tile_base = (int2*)(ws + L.tile_base);
+    c.tile_off = (int2*)(ws + L.tile_off);
     c.acc = (long long*)(ws + L.acc);
     c.stage_uid = (uint32_t*)(ws + L.stage_uid);
     c.stage_round = (uint32_t*)(ws + L.stage_round);
@@ -932,14 +1058,20 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         }
     }
     prof_mark(stream);
-    if (nb > 0) tile_reduce_kernel<<<L.n_tiles, 128, 0, stream>>>(c);
-    tile_scan_kernel<<<1, 1024, 0, stream>>>(c);
+    if (L.n_scan_tiles == 0) {
+        scan_block_kernel<<<1, 1024, 0, stream>>>(c, c.seg_counts, c.seg_off, c.n_segs);
+    } else {
+        scan_reduce_kernel<<<L.n_scan_tiles, 256, 0, stream>>>(c);
+        scan_block_kernel<<<1, 1024, 0, stream>>>(c, c.tile_sums, c.tile_off, L.n_scan_tiles);
+        scan_down_kernel<<<L.n_scan_tiles, 1024, 0, stream>>>(c);
+    }
     prof_mark(stream);
     if (nb > 0) {
+        const int blocks = (int)ceil_div(L.n_segs, kShadeThreads / 32);
         switch (strategy) {
-        case VR_NAIVE: finalize_kernel<VR_NAIVE><<<L.n_tiles, kFinThreads, 0, stream>>>(c, sp); break;
-        case VR_WARP: finalize_kernel<VR_WARP><<<L.n_tiles, kFinThreads, 0, stream>>>(c, sp); break;
-        default: finalize_kernel<VR_SORT><<<L.n_tiles, kFinThreads, 0, stream>>>(c, sp); break;
+        case VR_NAIVE: shade_kernel<VR_NAIVE><<<blocks, kShadeThreads, 0, stream>>>(c, sp); break;
+        case VR_WARP: shade_kernel<VR_WARP><<<blocks, kShadeThreads, 0, stream>>>(c, sp); break;
+        default: shade_kernel<VR_SORT><<<blocks, kShadeThreads, 0, stream>>>(c, sp); break;
         }
     }
     prof_mark(stream);

@@ -1,0 +1,32 @@
+#!/usr/bin/env python
+"""Summarise an .ncu-rep (read here, no GPU needed): python scripts/ncu_summary.py file.ncu-rep"""
+import csv, subprocess, sys
+WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
+        'launch__registers_per_thread', 'launch__grid_size', 'launch__block_size', 'launch__occupancy_limit_shared_mem',
+        'launch__occupancy_limit_registers', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'smsp__inst_executed.sum', 'smsp__issue_active.avg.pct_of_peak_sustained_active',
+        'smsp__thread_inst_executed_per_inst_executed.ratio', 'smsp__cycles_active.avg',
+        'l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum', 'l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum',
+        'l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum', 'l1tex__t_requests_pipe_lsu_mem_global_op_st.sum',
+        'l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum', 'l1tex__data_pipe_lsu_wavefronts_mem_shared.sum',
+        'lts__t_sectors_op_read.sum', 'lts__t_sectors_op_write.sum', 'lts__t_sector_hit_rate.pct',
+        'l1tex__t_sector_hit_rate.pct', 'sm__cycles_elapsed.max']
+STALL = 'smsp__average_warp'
+def main(path):
+    out = subprocess.run(['ncu', '-i', path, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    for r in rows[2:]:
+        print('==', r[hdr.index('Kernel Name')] if 'Kernel Name' in hdr else '')
+        stalls = []
+        for i, h in enumerate(hdr):
+            if h in WANT:
+                print(f'  {h:70s} {r[i]:>18s} {units[i]}')
+            if 'warp_issue_stalled' in h and h.endswith('_per_warp_active.pct'):
+                try: stalls.append((float(r[i]), h.split('stalled_')[1].replace('_per_warp_active.pct', '')))
+                except ValueError: pass
+        print('  top stalls (% of warp-active cycles):', ', '.join(f'{n} {v:.0f}' for v, n in sorted(stalls, reverse=True)[:6]))
+if __name__ == '__main__':
+    for p in sys.argv[1:]:
+        main(p)
