@@ -253,7 +253,7 @@ def main():
 
         def step():
             return engine.run_device(wl["strategy"], d_idx, offs[:-1], offs[1:], nb, n_idx, max_span, cfg,
-                                     hcfg, spec, buffers=bufs)
+                                     hcfg, spec, buffers=bufs, static=wl["batching"].startswith("static"))
 
         for _ in range(warmup):
             run = step()
@@ -342,7 +342,7 @@ def main():
             d_idx2.copy_(h_idx, non_blocking=True)
             pos42.copy_(h_pos, non_blocking=True)
             r = engine.run_device(wl["strategy"], d_idx2, offs[:-1], offs[1:], nb, n_idx, max_span, cfg, hcfg,
-                                  spec2, buffers=bufs)
+                                  spec2, buffers=bufs, static=wl["batching"].startswith("static"))
             h_stats.copy_(r.stats_dev, non_blocking=True)
             return r
 

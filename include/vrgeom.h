@@ -50,6 +50,10 @@ enum vr_strategy {
  * (batch_end[b] == batch_begin[b+1], e.g. any offsets array of batching.py:128-137):
  * the span scan is skipped.  The kernels verify the claim and report VR_ERR_BAD_BATCH. */
 #define VR_FLAG_CONTIGUOUS 0x200
+/* OR into `strategy` when the batches are static_batches(n, cfg) (batching.py:76-84):
+ * batch_begin[b] = batch_begin[0] + b * cfg->batch_size, last batch possibly shorter.  Implies
+ * VR_FLAG_CONTIGUOUS and selects the position-aligned kernels; verified on the device. */
+#define VR_FLAG_STATIC 0x400
 
 enum vr_status {
     VR_OK = 0,

@@ -17,6 +17,7 @@ STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_
 
 VR_FLAG_NO_BUDGET = 0x100
 VR_FLAG_CONTIGUOUS = 0x200
+VR_FLAG_STATIC = 0x400
 
 VR_SHADER_NONE, VR_SHADER_IDENTITY, VR_SHADER_POSITION = range(3)
 

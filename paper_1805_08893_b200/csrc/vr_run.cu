@@ -336,6 +336,210 @@ __global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
 }
 
 // ---------------------------------------------------------------------------------
+// K1 (warp voting), static-batch fast path: primitive_size 3, batch_size % 8 == 0 and
+// begin[b] = begin[0] + b * batch_size (batching.py:76-84).  Same closed form as above,
+// with everything position-aligned so that the whole warp stays converged:
+//   * every lane streams its batch as 16-byte loads, one group of 8 slots ahead, into two
+//     alternating register sets (no shared memory and no register moves on the index path);
+//   * the <= 2 index slots of a round's discarded tail are re-claimed in place when the round
+//     ends (they are the first slots of the next round), so the cursor never moves backwards;
+//   * local indices accumulate in registers, 8 per 16-byte store; a round's claims leave the
+//     shared claim array as 16-byte stores when the round ends.
+// Shared memory per lane: claims u32[W] + table u8[2W] = 192 B at W = 32.
+// ---------------------------------------------------------------------------------
+constexpr int kFastThreads = 128;
+
+template <int W>
+__global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int bs) {
+    constexpr int S = 2 * W;
+    constexpr int LOG2W = W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : W == 32 ? 5 : 6;
+    constexpr int LOG2S = LOG2W + 1;
+    constexpr uint32_t kRankMask = W - 1;
+    constexpr uint32_t kTagFree = (1u << (8 - LOG2W)) - 1;
+    constexpr int T = kFastThreads;
+    // shared memory: claims u32 [W][T] | table u8 [S] per thread as words [S/4][T]
+    // (tag << LOG2W | rank): every access stays inside the lane's own 32-bit column
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int t = threadIdx.x;
+    asm volatile("" : "+r"(t));
+    const int lane = t & 31;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
+    const uint32_t a_claims = sbase + 4 * t;
+    const uint32_t a_table = sbase + 4 * T * W + 4 * t;
+    auto tab = [&](uint32_t h) { return a_table + 4 * T * (h >> 2) + (h & 3); };
+    const int b = blockIdx.x * T + t;
+#pragma unroll
+    for (int h = 0; h < S / 4; h++) sts_u32(a_table + 4 * T * h, 0xFFFFFFFFu);
+    bool active = b < c.n_batches && !c.acc[ACC_ABORT];
+    int begin = 0, n = 0;
+    if (active && !validate_batch(c, b, begin, n)) { c.counts[b] = make_int2(0, 0); active = false; }
+    if (active && (begin - __ldg(c.bbegin) != b * bs || (n != bs && b != c.n_batches - 1) || (begin & 3))) {
+        report_error(c, b, VR_ERR_BAD_BATCH);  // not the static batching this path was promised
+        c.counts[b] = make_int2(0, 0);
+        active = false;
+    }
+    if (!active) n = 0;
+    const int mo = b * bs;
+    uint16_t* __restrict__ amap = (active && c.out.d_assembly_map) ? c.out.d_assembly_map + mo : nullptr;
+    uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
+    uint32_t* __restrict__ srd = c.stage_round + stage_round_base(c, b, mo);
+    const uint32_t* __restrict__ ids = c.idx + begin;
+    const int n_idx = (int)c.n_idx;
+
+    auto load_quad = [&](int q) -> uint4 {  // indices 4q..4q+3 of this lane's batch
+        const int g = begin + 4 * q;
+        if (4 * q + 4 <= n || (4 * q < n && g + 4 <= n_idx)) return __ldg(reinterpret_cast<const uint4*>(ids) + q);
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (4 * q + 0 < n) v.x = __ldg(ids + 4 * q + 0);
+        if (4 * q + 1 < n) v.y = __ldg(ids + 4 * q + 1);
+        if (4 * q + 2 < n) v.z = __ldg(ids + 4 * q + 2);
+        return v;
+    };
+
+    int fill = 0, cursor = 0, stop = n, rounds = 0, inv = 0;
+    uint32_t tagno = 0;
+    uint32_t h = 0;  // free slot found by the last failed lookup
+
+    auto lookup = [&](uint32_t x) -> int {
+        h = (x * 0x9E3779B1u) >> (32 - LOG2S);
+        for (;;) {
+            const uint32_t ent = lds_u8(tab(h));
+            if ((ent >> LOG2W) != tagno) return -1;  // free: never used or from an earlier round
+            const uint32_t rr = ent & kRankMask;
+            if (lds_u32(a_claims + 4 * T * rr) == x) return (int)rr;
+            h = (h + 1) & (S - 1);
+        }
+    };
+    auto claim = [&](uint32_t x, int p) -> int {  // strategies.py:207-212
+        sts_u32(a_claims + 4 * T * fill, x);
+        sts_u8(tab(h), (tagno << LOG2W) | (uint32_t)fill);
+        const int r = fill++;
+        if (fill == W) stop = min(n, cursor + ((p - cursor) / W + 1) * W);  // end of this fetch
+        return r;
+    };
+    auto flush_claims = [&]() {  // the round's claims, 16 bytes at a time (inv % 4 == 0)
+        for (int j = 0; j < fill; j += 4) {
+            uint4 v;
+            v.x = lds_u32(a_claims + 4 * T * (j + 0));
+            v.y = lds_u32(a_claims + 4 * T * ((j + 1) & (W - 1)));
+            v.z = lds_u32(a_claims + 4 * T * ((j + 2) & (W - 1)));
+            v.w = lds_u32(a_claims + 4 * T * ((j + 3) & (W - 1)));
+            *reinterpret_cast<uint4*>(suid + inv + j) = v;
+        }
+    };
+
+    uint32_t r[8];                       // local indices of the current group of 8 slots
+    uint4 gp = make_uint4(0, 0, 0, 0);   // previous group, packed, not yet stored
+    uint32_t px6 = 0, px7 = 0;           // last two ids of the previous group
+    auto store_group = [&](int kg, const uint4& g) {  // 8 local indices = one 16-byte store
+        if (!amap || 8 * kg >= n) return;
+        if (8 * kg + 8 <= n) {
+            *reinterpret_cast<uint4*>(amap + 8 * kg) = g;
+        } else {
+            const uint32_t w4[4] = {g.x, g.y, g.z, g.w};
+            for (int e = 0; e < 8 && 8 * kg + e < n; e++)
+                amap[8 * kg + e] = (uint16_t)(w4[e >> 1] >> (16 * (e & 1)));
+        }
+    };
+
+    // one group of 8 index slots; a round end inside the group is handled once, then the
+    // group resumes at the slot that closed the round
+    auto process_group = [&](const int k, const uint4& qa, const uint4& qb) {
+        const uint32_t xs[8] = {qa.x, qa.y, qa.z, qa.w, qb.x, qb.y, qb.z, qb.w};
+        int e0 = 0;
+        for (;;) {
+            int pe = -1;  // slot of this group before which the current round ends
+#pragma unroll
+            for (int e = 0; e < 8; e++) {
+                const int p = 8 * k + e;
+                if (e >= e0 && pe < 0 && p < n) {
+                    int rr = -1;
+                    if (p < stop) {  // else: the fetch that filled the warp is exhausted
+                        rr = lookup(xs[e]);
+                        if (rr < 0 && fill < W) rr = claim(xs[e], p);
+                    }
+                    if (rr < 0) pe = e;  // p >= stop, or first unassignable slot
+                    else r[e] = (uint32_t)rr;
+                }
+                if (e == 1 && k > 0 && pe < 0 && e0 <= 1) store_group(k - 1, gp);  // slots < 8k are final now
+            }
+            if (pe < 0) break;
+            // strategies.py:220-231: the round ends before slot p; emit whole primitives, re-open
+            // at the first unconsumed slot and give the discarded tail its claims of the new round
+            const int p = 8 * k + pe;
+            const int emitted = (p - cursor) / 3;
+            const int consumed = cursor + 3 * emitted;
+            flush_claims();
+            srd[rounds++] = ((uint32_t)emitted << 8) | (uint32_t)fill;
+            inv += fill;
+            fill = 0;
+            cursor = consumed;
+            stop = n;
+            if (++tagno == kTagFree) {
+                for (int hh = 0; hh < S / 4; hh++) sts_u32(a_table + 4 * T * hh, 0xFFFFFFFFu);
+                tagno = 0;
+            }
+            for (int tp = consumed; tp < p; tp++) {
+                uint32_t id = (tp & 7) == 6 ? px6 : px7;
+                if ((tp >> 3) == k) {
+#pragma unroll
+                    for (int e = 0; e < 8; e++)
+                        if ((tp & 7) == e) id = xs[e];
+                }
+                int rr = lookup(id);
+                if (rr < 0) rr = claim(id, tp);
+                if ((tp >> 3) == k) {
+#pragma unroll
+                    for (int e = 0; e < 8; e++)
+                        if ((tp & 7) == e) r[e] = (uint32_t)rr;
+                } else if ((tp & 7) == 6) {
+                    gp.w = (gp.w & 0xFFFF0000u) | (uint32_t)rr;
+                } else {
+                    gp.w = (gp.w & 0x0000FFFFu) | ((uint32_t)rr << 16);
+                }
+            }
+            if (pe <= 1 && k > 0) store_group(k - 1, gp);  // tail fixed: the previous group is final
+            e0 = pe;
+        }
+        gp = make_uint4(r[0] | (r[1] << 16), r[2] | (r[3] << 16), r[4] | (r[5] << 16), r[6] | (r[7] << 16));
+        px6 = xs[6];
+        px7 = xs[7];
+    };
+
+    const int groups = (bs + 7) >> 3;
+#pragma unroll
+    for (int e = 0; e < 8; e++) r[e] = 0;
+    uint4 a0 = load_quad(0), a1 = load_quad(1);
+    for (int k = 0; k < groups; k += 2) {
+        const uint4 b0 = load_quad(2 * k + 2), b1 = load_quad(2 * k + 3);
+        process_group(k, a0, a1);
+        if (k + 1 < groups) {
+            a0 = load_quad(2 * k + 4);
+            a1 = load_quad(2 * k + 5);
+            process_group(k + 1, b0, b1);
+        }
+    }
+    int seg_r = 0, seg_u = 0;
+    if (active) {
+        // last group, then the final round (the batch end closes it; nothing is discarded)
+        store_group(groups - 1, gp);
+        flush_claims();
+        srd[rounds++] = ((uint32_t)((n - cursor) / 3) << 8) | (uint32_t)fill;
+        inv += fill;
+        c.counts[b] = make_int2(rounds, inv);
+        seg_r = rounds;
+        seg_u = inv;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        seg_r += __shfl_xor_sync(0xffffffffu, seg_r, d);
+        seg_u += __shfl_xor_sync(0xffffffffu, seg_u, d);
+    }
+    const int seg = b >> 5;
+    if (lane == 0 && seg < c.n_segs) c.seg_counts[seg] = make_int2(seg_r, seg_u);
+}
+
+// ---------------------------------------------------------------------------------
 // K1 (sort): strategies.py:235-260 -- Algorithm 2.  One CTA per batch: bitonic sort of
 // (id << 32 | slot) keys in shared memory (the slot in the low half makes it the stable
 // sort the reference asks for), run-head marks, CTA exclusive scan -> ranks, unique ids in
@@ -835,6 +1039,15 @@ static int launch_warp_tpb(const RunCtx& c, cudaStream_t stream) {
     return VR_OK;
 }
 
+template <int W>
+static int launch_warp_fast(const RunCtx& c, int bs, cudaStream_t stream) {
+    const size_t smem = (size_t)kFastThreads * (4 * W + 2 * W);
+    if (smem > 48 * 1024)
+        VR_CUDA_CHECK(cudaFuncSetAttribute(warp_fast_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    warp_fast_kernel<W><<<(int)ceil_div(c.n_batches, kFastThreads), kFastThreads, smem, stream>>>(c, bs);
+    return VR_OK;
+}
+
 }  // namespace vr
 
 using namespace vr;
@@ -961,7 +1174,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
            int64_t nb, int64_t span_total, int32_t max_span, const vr_batch_config* cfg, const vr_hash_config* hcfg,
            const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_) {
     const bool no_budget = (strategy & VR_FLAG_NO_BUDGET) != 0;
-    const bool contiguous = (strategy & VR_FLAG_CONTIGUOUS) != 0;
+    const bool static_batches = (strategy & VR_FLAG_STATIC) != 0;
+    const bool contiguous = (strategy & VR_FLAG_CONTIGUOUS) != 0 || static_batches;
     strategy &= 0xFF;
     if (strategy < VR_NAIVE || strategy > VR_PHASH) return VR_ERR_UNKNOWN_STRATEGY;  // strategies.py:422-423
     int st = vr_check_batch_config(cfg);
@@ -1042,6 +1256,16 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (nb > 0) {
         if (strategy == VR_NAIVE) {
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
+        } else if (strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0) {
+            const int bs = cfg->batch_size;
+            switch (cfg->warp_width) {
+            case 4: st = launch_warp_fast<4>(c, bs, stream); break;
+            case 8: st = launch_warp_fast<8>(c, bs, stream); break;
+            case 16: st = launch_warp_fast<16>(c, bs, stream); break;
+            case 32: st = launch_warp_fast<32>(c, bs, stream); break;
+            default: st = launch_warp_fast<64>(c, bs, stream); break;
+            }
+            if (st) return st;
         } else if (strategy == VR_WARP) {
             switch (cfg->warp_width) {
             case 4: st = launch_warp_tpb<4>(c, stream); break;

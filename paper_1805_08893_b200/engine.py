@@ -103,6 +103,7 @@ def static_offsets_device(index_count: int, cfg: BatchConfig, device=None) -> to
     offs = torch.empty(nb + 1, dtype=torch.int32, device=dev)
     with torch.cuda.device(dev):
         raise_status(lib.vr_static_offsets(index_count, C.byref(c), _ptr(offs), _stream_ptr()))
+    offs.vr_static_batch_size = cfg.batch_size  # lets the runner pick the position-aligned kernels
     return offs
 
 
@@ -253,7 +254,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                n_batches: int, span_total: int, max_span: int, cfg: BatchConfig, hcfg=None,
                shader: ShaderSpec | None = None, *, want_counts: bool = False,
                buffers: RunBuffers | None = None, enforce_budget: bool = True,
-               contiguous: bool | None = None) -> DeviceRun:
+               contiguous: bool | None = None, static: bool = False) -> DeviceRun:
     """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back."""
     lib = N.require_cuda()
     if strategy not in N.STRATEGY_IDS:
@@ -263,7 +264,8 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
     if contiguous is None:  # begin/end are two views of one offsets array
         contiguous = (n_batches > 0 and d_begin.data_ptr() + 4 == d_end.data_ptr()
                       and d_begin.is_contiguous() and d_end.is_contiguous())
-    flags = (0 if enforce_budget else N.VR_FLAG_NO_BUDGET) | (N.VR_FLAG_CONTIGUOUS if contiguous else 0)
+    flags = ((0 if enforce_budget else N.VR_FLAG_NO_BUDGET) | (N.VR_FLAG_CONTIGUOUS if contiguous else 0)
+             | (N.VR_FLAG_STATIC if static else 0))
     shader = shader or ShaderSpec()
     buffers = buffers or RunBuffers()
     c = _cfg_c(cfg)

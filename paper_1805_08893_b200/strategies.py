@@ -316,6 +316,7 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
         max_span = max(cfg.batch_size, cfg.max_indices)
         span_total = n_idx
         contiguous = True
+        static = getattr(batches, "vr_static_batch_size", None) == cfg.batch_size
     else:
         nb = len(batches)
         if nb:
@@ -328,6 +329,8 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
             max_span = int((be - bb).max())
             span_total = int((be - bb).sum())
             contiguous = bool((bb[1:] == be[:-1]).all())
+            static = bool(contiguous and (np.diff(bb) == cfg.batch_size).all()
+                          and (be[-1] - bb[-1]) <= cfg.batch_size and (nb == 1 or bb[1] - bb[0] == cfg.batch_size))
 
     if strategy in ("hash", "phash"):
         hash_cfg = hash_cfg or HashConfig(table_size=cfg.block_size)  # strategies.py:431
@@ -357,7 +360,7 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
         d_begin, d_end = both[0], both[1]
     spec, positions = _shader_spec(shader, dev, vertex_count)
     run = engine.run_device(strategy, d_idx, d_begin, d_end, nb, span_total, max_span, cfg, hash_cfg,
-                            spec, want_counts=vertex_count is not None, contiguous=contiguous)
+                            spec, want_counts=vertex_count is not None, contiguous=contiguous, static=static)
     run.check()
 
     shade_counts = None
