@@ -357,15 +357,17 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
     constexpr uint32_t kRankMask = W - 1;
     constexpr uint32_t kTagFree = (1u << (8 - LOG2W)) - 1;
     constexpr int T = kFastThreads;
-    // shared memory: claims u32 [W][T] | table u8 [S] per thread as words [S/4][T]
-    // (tag << LOG2W | rank): every access stays inside the lane's own 32-bit column
+    // shared memory: index quads uint4 [4][T] (cp.async ring) | claims u32 [W][T] | table u8 [S]
+    // per thread as words [S/4][T] (tag << LOG2W | rank): every access stays inside the lane's
+    // own column
     extern __shared__ __align__(16) unsigned char smem_raw[];
     int t = threadIdx.x;
     asm volatile("" : "+r"(t));
     const int lane = t & 31;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    const uint32_t a_claims = sbase + 4 * t;
-    const uint32_t a_table = sbase + 4 * T * W + 4 * t;
+    const uint32_t a_quads = sbase + 16 * t;
+    const uint32_t a_claims = sbase + 64 * T + 4 * t;
+    const uint32_t a_table = sbase + 64 * T + 4 * T * W + 4 * t;
     auto tab = [&](uint32_t h) { return a_table + 4 * T * (h >> 2) + (h & 3); };
     const int b = blockIdx.x * T + t;
 #pragma unroll
@@ -384,16 +386,12 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
     uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
     uint32_t* __restrict__ srd = c.stage_round + stage_round_base(c, b, mo);
     const uint32_t* __restrict__ ids = c.idx + begin;
-    const int n_idx = (int)c.n_idx;
 
-    auto load_quad = [&](int q) -> uint4 {  // indices 4q..4q+3 of this lane's batch
-        const int g = begin + 4 * q;
-        if (4 * q + 4 <= n || (4 * q < n && g + 4 <= n_idx)) return __ldg(reinterpret_cast<const uint4*>(ids) + q);
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (4 * q + 0 < n) v.x = __ldg(ids + 4 * q + 0);
-        if (4 * q + 1 < n) v.y = __ldg(ids + 4 * q + 1);
-        if (4 * q + 2 < n) v.z = __ldg(ids + 4 * q + 2);
-        return v;
+    // indices 4q..4q+3 of this lane's batch -> ring slot q & 3 (zero-filled past the batch end)
+    auto issue_quad = [&](int q) {
+        const int rem = n - 4 * q;
+        const int bytes = rem >= 4 ? 16 : (rem > 0 ? 4 * rem : 0);
+        cp_async16(a_quads + 16 * T * (q & 3), bytes ? ids + 4 * q : c.idx, bytes);
     };
 
     int fill = 0, cursor = 0, stop = n, rounds = 0, inv = 0;
@@ -509,16 +507,18 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
     const int groups = (bs + 7) >> 3;
 #pragma unroll
     for (int e = 0; e < 8; e++) r[e] = 0;
-    uint4 a0 = load_quad(0), a1 = load_quad(1);
-    for (int k = 0; k < groups; k += 2) {
-        const uint4 b0 = load_quad(2 * k + 2), b1 = load_quad(2 * k + 3);
-        process_group(k, a0, a1);
-        if (k + 1 < groups) {
-            a0 = load_quad(2 * k + 4);
-            a1 = load_quad(2 * k + 5);
-            process_group(k + 1, b0, b1);
-        }
+    issue_quad(0);
+    issue_quad(1);
+    cp_async_commit();
+    for (int k = 0; k < groups; k++) {
+        issue_quad(2 * k + 2);  // one group ahead
+        issue_quad(2 * k + 3);
+        cp_async_commit();
+        cp_async_wait<1>();
+        const uint4 qa = lds_u128(a_quads + 16 * T * ((2 * k) & 3)), qb = lds_u128(a_quads + 16 * T * ((2 * k + 1) & 3));
+        process_group(k, qa, qb);
     }
+    cp_async_wait<0>();
     int seg_r = 0, seg_u = 0;
     if (active) {
         // last group, then the final round (the batch end closes it; nothing is discarded)
@@ -756,30 +756,42 @@ __device__ void finish_stats(const RunCtx& c, long long R, long long U) {
 }
 
 __global__ void __launch_bounds__(1024) scan_block_kernel(RunCtx c, const int2* __restrict__ in, int2* __restrict__ out, int n) {
-    __shared__ int scratch[40];
-    __shared__ int chunk_r[1024];
-    __shared__ int chunk_u[1024];
-    __shared__ long long carry_r, carry_u;
-    const int tid = threadIdx.x;
-    if (tid == 0) { carry_r = 0; carry_u = 0; }
-    __syncthreads();
-    for (int base = 0; base < n; base += 1024) {
-        int k = base + tid;
-        int2 v = k < n ? in[k] : make_int2(0, 0);
-        chunk_r[tid] = v.x;
-        chunk_u[tid] = v.y;
-        __syncthreads();
-        int tr = block_exclusive_scan(chunk_r, 1024, scratch);
-        int tu = block_exclusive_scan(chunk_u, 1024, scratch);
-        long long br = carry_r, bu = carry_u;
-        if (k < n) out[k] = make_int2((int)min(br + chunk_r[tid], 0x7fffffffLL), (int)min(bu + chunk_u[tid], 0x7fffffffLL));
-        __syncthreads();
-        if (tid == 0) { carry_r = br + tr; carry_u = bu + tu; }
-        __syncthreads();
+    __shared__ long long wr[32], wu[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (n + 1023) >> 10;
+    const int lo = min(n, tid * per), hi = min(n, lo + per);
+    long long r = 0, u = 0;
+    for (int k = lo; k < hi; k++) { const int2 v = in[k]; r += v.x; u += v.y; }
+    long long ir = r, iu = u;  // inclusive scan over the CTA's 1024 partial sums
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long tr = __shfl_up_sync(0xffffffffu, ir, d), tu = __shfl_up_sync(0xffffffffu, iu, d);
+        if (lane >= d) { ir += tr; iu += tu; }
     }
-    if (tid == 0) {
-        out[n] = make_int2((int)min((long long)carry_r, 0x7fffffffLL), (int)min((long long)carry_u, 0x7fffffffLL));
-        finish_stats(c, carry_r, carry_u);
+    if (lane == 31) { wr[wid] = ir; wu[wid] = iu; }
+    __syncthreads();
+    if (wid == 0) {
+        long long xr = wr[lane], xu = wu[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long tr = __shfl_up_sync(0xffffffffu, xr, d), tu = __shfl_up_sync(0xffffffffu, xu, d);
+            if (lane >= d) { xr += tr; xu += tu; }
+        }
+        wr[lane] = xr;
+        wu[lane] = xu;
+    }
+    __syncthreads();
+    long long br = (wid ? wr[wid - 1] : 0) + ir - r, bu = (wid ? wu[wid - 1] : 0) + iu - u;
+    for (int k = lo; k < hi; k++) {
+        const int2 v = in[k];
+        out[k] = make_int2((int)min(br, 0x7fffffffLL), (int)min(bu, 0x7fffffffLL));
+        br += v.x;
+        bu += v.y;
+    }
+    if (tid == 1023) {
+        const long long R = wr[31], U = wu[31];
+        out[n] = make_int2((int)min(R, 0x7fffffffLL), (int)min(U, 0x7fffffffLL));
+        finish_stats(c, R, U);
     }
 }
 
@@ -895,15 +907,51 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
                 run += (int)(w & 0xFFu);
             }
         }
-        // unique ids: each half-warp streams one batch at a time (a batch holds ~W ids)
+        // unique ids: flat over the segment's outputs, 32 per step.  The owner batch of an output
+        // comes from one warp-wide OR: lane L sets the bit of the last output of its batch, and an
+        // output's owner is the first owner of the step plus the number of batch ends before it.
         const unsigned long long my_src = (unsigned long long)(c.stage_uid + stage_uid_base(c, b, mo));
-        const int half = lane >> 4, l = lane & 15;
-        for (int pair = 0; pair < 16; pair++) {
-            const int L = 2 * pair + half;
-            const int n_b = __shfl_sync(0xffffffffu, cnt.y, L);
-            const int d_b = __shfl_sync(0xffffffffu, u0, L);
-            const uint32_t* src = (const uint32_t*)__shfl_sync(0xffffffffu, my_src, L);
-            shade_stream<STRATEGY>(c, sp, src, n_b, d_b, l, 16, 0);
+        const int ex = inc_u - cnt.y;
+        const int tot = __shfl_sync(0xffffffffu, inc_u, 31);
+        const bool want_uid = c.out.d_unique_ids != nullptr;
+        const bool want_pos = sp.kind == VR_SHADER_POSITION;
+        const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
+        const bool want_cnt = c.out.d_shade_counts != nullptr;
+        uint32_t* __restrict__ out_uid = c.out.d_unique_ids + off.y;
+        float4* __restrict__ shaded = reinterpret_cast<float4*>(c.out.d_shaded4) + off.y;
+        const uint32_t lt = (1u << lane) - 1;
+        int first_owner = 0;
+        for (int j0 = 0; j0 < tot; j0 += 32 * kShadeUnroll) {
+            uint32_t uid[kShadeUnroll];
+            float4 p[kShadeUnroll];
+#pragma unroll
+            for (int u = 0; u < kShadeUnroll; u++) {
+                const int jb = j0 + 32 * u;
+                const int d = inc_u - jb - 1;
+                const uint32_t ends = __reduce_or_sync(0xffffffffu, (cnt.y > 0 && d >= 0 && d < 32) ? (1u << d) : 0u);
+                const int owner = (first_owner + __popc(ends & lt)) & 31;
+                first_owner += __popc(ends);
+                const int oex = __shfl_sync(0xffffffffu, ex, owner);
+                const uint32_t* osrc = (const uint32_t*)__shfl_sync(0xffffffffu, my_src, owner);
+                const int j = jb + lane;
+                uid[u] = j < tot ? osrc[j - oex] : 0u;
+            }
+            if (want_pos) {
+#pragma unroll
+                for (int u = 0; u < kShadeUnroll; u++)
+                    if (j0 + 32 * u + lane < tot) p[u] = __ldg(sp.pos4 + uid[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < kShadeUnroll; u++) {
+                const int j = j0 + 32 * u + lane;
+                if (j >= tot) continue;
+                if (want_uid) out_uid[j] = uid[u];
+                if (want_pos) shaded[j] = transform_position(sp, p[u]);
+                if (want_attr)
+                    for (int k = 0; k < sp.attr_words; k++)
+                        c.out.d_shaded_attr[((int64_t)off.y + j) * sp.attr_words + k] = __ldg(sp.attr + (int64_t)uid[u] * sp.attr_words + k);
+                if (want_cnt) atomicAdd(&c.out.d_shade_counts[uid[u]], 1);
+            }
         }
     } else {
         const int b = s;
@@ -1041,7 +1089,7 @@ static int launch_warp_tpb(const RunCtx& c, cudaStream_t stream) {
 
 template <int W>
 static int launch_warp_fast(const RunCtx& c, int bs, cudaStream_t stream) {
-    const size_t smem = (size_t)kFastThreads * (4 * W + 2 * W);
+    const size_t smem = (size_t)kFastThreads * (64 + 4 * W + 2 * W);
     if (smem > 48 * 1024)
         VR_CUDA_CHECK(cudaFuncSetAttribute(warp_fast_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     warp_fast_kernel<W><<<(int)ceil_div(c.n_batches, kFastThreads), kFastThreads, smem, stream>>>(c, bs);
