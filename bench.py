@@ -306,12 +306,14 @@ def main():
             pass
         peak, peak_src = (peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)") if "hbm_gbs" in peaks \
             else (6650.0, "fallback (B200_PROFILING.md)")
+        launches = lib.vr_last_launch_count()
+        fused = launches == 2  # init + one kernel that dedups, places and shades
         dom = int(np.argmax(stage_ms))
         # per-kernel algorithmic bytes: dedup = index read + map write + metadata;
         # shade/finalize = staged id read is not algorithmic: position read + shaded write
         kernel_alg = {"dedup": 4 * n_idx + 2 * n_idx + 12 * nb, "shade_finalize": 32 * inv}
-        dom_name = N.PROFILE_STAGE_NAMES[dom]
-        dom_alg = kernel_alg.get(dom_name, alg)
+        dom_name = "fused dedup+offsets+shade" if fused else N.PROFILE_STAGE_NAMES[dom]
+        dom_alg = alg if fused else kernel_alg.get(dom_name, alg)
         res = {
             "value": value, "ms_per_step": ms_per_step, "wall_s": wall,
             "stage_ms": {N.PROFILE_STAGE_NAMES[i]: round(float(stage_ms[i]), 5) for i in range(N.VR_PROFILE_STAGES)},
@@ -325,7 +327,7 @@ def main():
                                "frac": alg / (ms_per_step * 1e-3) / 1e9 / peak},
             "invocations": inv, "shading_rate": inv / mesh.vertex_count, "reuse_rate": 1 - inv / n_idx,
             "batches": nb, "batch_formation_ms": t_form, "clocks": clocks.summary(),
-            "gpu_launches": steps * 5,
+            "gpu_launches": steps * launches, "fused": fused,
         }
         if not full:
             return res, None

@@ -54,6 +54,9 @@ enum vr_strategy {
  * batch_begin[b] = batch_begin[0] + b * cfg->batch_size, last batch possibly shorter.  Implies
  * VR_FLAG_CONTIGUOUS and selects the position-aligned kernels; verified on the device. */
 #define VR_FLAG_STATIC 0x400
+/* OR into `strategy` to keep dedup, offset scan and shading in separate kernels even where
+ * a fused kernel exists (ablation / debugging; results are identical). */
+#define VR_FLAG_NO_FUSE 0x800
 
 enum vr_status {
     VR_OK = 0,
@@ -196,6 +199,8 @@ int vr_expand_stream(const int32_t *d_batch_round_off, const int32_t *d_round_ui
  * vr_profile_read synchronises the last event and returns the number of stages written. */
 #define VR_PROFILE_STAGES 4
 int vr_profile_enable(int on);
+/* Number of kernels the last vr_run of this process launched (bench.py's gpu_launches). */
+int vr_last_launch_count(void);
 int vr_profile_read(float *ms, int cap);
 
 #ifdef __cplusplus

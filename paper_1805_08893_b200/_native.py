@@ -18,6 +18,7 @@ STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_
 VR_FLAG_NO_BUDGET = 0x100
 VR_FLAG_CONTIGUOUS = 0x200
 VR_FLAG_STATIC = 0x400
+VR_FLAG_NO_FUSE = 0x800
 
 VR_SHADER_NONE, VR_SHADER_IDENTITY, VR_SHADER_POSITION = range(3)
 
@@ -76,6 +77,7 @@ _SIGNATURES = {
                          C.c_int32, C.POINTER(BatchConfigC), C.POINTER(HashConfigC), C.POINTER(ShaderC),
                          C.POINTER(OutputsC), C.c_void_p, C.c_size_t, C.c_void_p]),
     "vr_profile_enable": (C.c_int, [C.c_int]),
+    "vr_last_launch_count": (C.c_int, []),
     "vr_profile_read": (C.c_int, [C.POINTER(C.c_float), C.c_int]),
     "vr_expand_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,

@@ -17,7 +17,7 @@
 
 namespace vr {
 
-enum { ACC_PROBES_FAST = 0, ACC_PROBES_SLOW, ACC_MAX_CHAIN, ACC_ERROR, ACC_ABORT, ACC_WORDS = 8 };
+enum { ACC_PROBES_FAST = 0, ACC_PROBES_SLOW, ACC_MAX_CHAIN, ACC_ERROR, ACC_ABORT, ACC_TICKET, ACC_WORDS = 8 };
 
 struct RunCtx {
     const uint32_t* __restrict__ idx;
@@ -49,6 +49,8 @@ struct RunCtx {
     uint32_t* stage_uid;    // staged unique ids
     uint32_t* stage_round;  // staged round records: primitives << 8 | claims (warp)
     long long* acc;         // [ACC_WORDS]
+    unsigned long long* tile_state;  // [n_fused_tiles] decoupled look-back: flag<<62 | rounds<<32 | ids
+    int n_fused_tiles;
     // outputs
     vr_outputs out;
 };
@@ -86,7 +88,9 @@ __device__ __forceinline__ bool validate_batch(const RunCtx& c, int b, int& begi
 // K0
 // ---------------------------------------------------------------------------------
 __global__ void init_kernel(RunCtx c) {
-    if (threadIdx.x < ACC_WORDS) c.acc[threadIdx.x] = 0;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < ACC_WORDS) c.acc[i] = 0;
+    if (i < c.n_fused_tiles) c.tile_state[i] = 0ull;
 }
 
 // Non-contiguous batch lists: single-CTA scan of the spans (general path, not the hot one).
@@ -335,6 +339,33 @@ __global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
     if ((t & 31) == 0 && seg < c.n_segs) c.seg_counts[seg] = make_int2(seg_r, seg_u);
 }
 
+// Totals, statistics and the closing table entries (strategies.py:472-502); one thread.
+__device__ void finish_stats(const RunCtx& c, long long R, long long U) {
+    int64_t* st = c.out.d_stats;
+    for (int i = 0; i < VR_STATS_WORDS; i++) st[i] = 0;
+    long long span_total = 0;
+    if (c.n_batches > 0)
+        span_total = c.contiguous ? (long long)c.bend[c.n_batches - 1] - c.bbegin[0] : c.map_off[c.n_batches];
+    if (span_total > c.span_cap) report_error(c, 0, VR_ERR_CAPACITY);
+    if (U > c.out.cap_unique || R > c.out.cap_rounds || U > 0x7fffffffLL) report_error(c, 0, VR_ERR_CAPACITY);
+    st[VR_STAT_INDICES] = span_total;
+    st[VR_STAT_INVOCATIONS] = U;
+    st[VR_STAT_BATCHES] = c.n_batches;
+    st[VR_STAT_ROUNDS] = R;
+    st[VR_STAT_PROBES_FAST] = c.acc[ACC_PROBES_FAST];
+    st[VR_STAT_PROBES_SLOW] = c.acc[ACC_PROBES_SLOW];
+    st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
+    const long long e = c.acc[ACC_ERROR];
+    if (e == 0) {
+        st[VR_STAT_ERROR] = -1;
+        if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
+        if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
+    } else {
+        st[VR_STAT_ERROR] = ((0x7FFFFFFFFFFFLL - (e >> 8)) << 8) | (e & 0xFF);
+        c.acc[ACC_ABORT] = 1;  // K3 must not touch the outputs
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // K1 (warp voting), static-batch fast path: primitive_size 3, batch_size % 8 == 0 and
 // begin[b] = begin[0] + b * batch_size (batching.py:76-84).  Same closed form as above,
@@ -349,8 +380,14 @@ __global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
 // ---------------------------------------------------------------------------------
 constexpr int kFastThreads = 128;
 
-template <int W>
-__global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int bs) {
+// FUSED: the same CTA goes on to place and shade its own unique ids.  Output offsets come from a
+// decoupled look-back over CTA tiles (tiles are handed out by an atomic ticket, so every
+// predecessor of a tile is resident or finished): while some warps of an SM wait on gathers
+// in the shading phase, others are busy with the (latency-bound) dedup phase.
+constexpr unsigned long long kStateAggregate = 1ull << 62, kStateInclusive = 2ull << 62;
+
+template <int W, bool FUSED>
+__global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int bs, ShaderParams sp) {
     constexpr int S = 2 * W;
     constexpr int LOG2W = W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : W == 32 ? 5 : 6;
     constexpr int LOG2S = LOG2W + 1;
@@ -369,7 +406,16 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
     const uint32_t a_claims = sbase + 64 * T + 4 * t;
     const uint32_t a_table = sbase + 64 * T + 4 * T * W + 4 * t;
     auto tab = [&](uint32_t h) { return a_table + 4 * T * (h >> 2) + (h & 3); };
-    const int b = blockIdx.x * T + t;
+    __shared__ int s_tile;
+    __shared__ int2 s_warp_tot[T / 32];
+    __shared__ int2 s_base;
+    int tile = blockIdx.x;
+    if (FUSED) {  // tiles in ticket order
+        if (t == 0) s_tile = (int)atomicAdd((unsigned long long*)&c.acc[ACC_TICKET], 1ull);
+        __syncthreads();
+        tile = s_tile;
+    }
+    const int b = tile * T + t;
 #pragma unroll
     for (int h = 0; h < S / 4; h++) sts_u32(a_table + 4 * T * h, 0xFFFFFFFFu);
     bool active = b < c.n_batches && !c.acc[ACC_ABORT];
@@ -535,8 +581,126 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
         seg_r += __shfl_xor_sync(0xffffffffu, seg_r, d);
         seg_u += __shfl_xor_sync(0xffffffffu, seg_u, d);
     }
-    const int seg = b >> 5;
-    if (lane == 0 && seg < c.n_segs) c.seg_counts[seg] = make_int2(seg_r, seg_u);
+    if (!FUSED) {
+        const int seg = b >> 5;
+        if (lane == 0 && seg < c.n_segs) c.seg_counts[seg] = make_int2(seg_r, seg_u);
+        return;
+    }
+    // ---- output offsets: CTA aggregate, then decoupled look-back by warp 0
+    const int wid = t >> 5;
+    if (lane == 0) s_warp_tot[wid] = make_int2(seg_r, seg_u);
+    __syncthreads();
+    if (wid == 0) {
+        int ar = 0, au = 0;
+#pragma unroll
+        for (int w = 0; w < T / 32; w++) { ar += s_warp_tot[w].x; au += s_warp_tot[w].y; }
+        volatile unsigned long long* state = c.tile_state;
+        if (lane == 0) {
+            __threadfence();  // errors reported by this tile are visible before its state
+            state[tile] = kStateAggregate | ((unsigned long long)(uint32_t)ar << 32) | (uint32_t)au;
+        }
+        long long er = 0, eu = 0;  // exclusive prefix of this tile
+        bool lost = false;
+        for (int p = tile - 1; p >= 0; p -= 32) {
+            const int idx = p - lane;
+            unsigned long long word = kStateInclusive;  // tiles before the first one: inclusive zero
+            int spins = 0;
+            for (;;) {
+                if (idx >= 0) word = state[idx];
+                if (!__any_sync(0xffffffffu, (word >> 62) == 0)) break;
+                if (++spins > (1 << 20)) { lost = true; break; }
+                __nanosleep(40);
+            }
+            if (lost) break;
+            const uint32_t incl = __ballot_sync(0xffffffffu, (word >> 62) == 2);
+            const int upto = incl ? __ffs(incl) - 1 : 31;  // nearest predecessor holding an inclusive prefix
+            long long vr = lane <= upto ? (long long)((word >> 32) & 0x3FFFFFFFull) : 0;
+            long long vu = lane <= upto ? (long long)(word & 0xFFFFFFFFull) : 0;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                vr += __shfl_xor_sync(0xffffffffu, vr, d);
+                vu += __shfl_xor_sync(0xffffffffu, vu, d);
+            }
+            er += vr;
+            eu += vu;
+            if (incl) break;
+        }
+        if (lane == 0) {
+            if (lost) report_error(c, (int64_t)tile * T, VR_ERR_CUDA);
+            const long long R = er + ar, U = eu + au;
+            state[tile] = kStateInclusive | ((unsigned long long)(R & 0x3FFFFFFF) << 32) | (unsigned long long)(U & 0xFFFFFFFFll);
+            const bool fits = U <= c.out.cap_unique && R <= c.out.cap_rounds && U <= 0x7fffffffLL && !lost;
+            if (!fits) report_error(c, (int64_t)tile * T, VR_ERR_CAPACITY);
+            s_base = fits ? make_int2((int)er, (int)eu) : make_int2(-1, -1);
+            if (tile == c.n_fused_tiles - 1) { __threadfence(); finish_stats(c, R, U); }
+        }
+    }
+    __syncthreads();
+    int2 off = s_base;
+    if (off.x < 0) return;  // offsets unknown or outputs too small: leave them untouched
+    for (int w = 0; w < wid; w++) { off.x += s_warp_tot[w].x; off.y += s_warp_tot[w].y; }
+
+    // ---- this warp's segment: round tables, then unique ids + shading (as in shade_kernel)
+    {
+        const int my_r = active ? rounds : 0, my_u = active ? inv : 0;
+        const int inc_r = warp_incl_scan(my_r, lane), inc_u = warp_incl_scan(my_u, lane);
+        const int u0 = off.y + inc_u - my_u;
+        if (active) {
+            const int r0 = off.x + inc_r - my_r;
+            int run = u0;
+            if (c.out.d_batch_round_off) c.out.d_batch_round_off[b] = r0;
+            for (int q = 0; q < my_r; q++) {
+                const uint32_t wv = srd[q];
+                if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0 + q] = run;
+                if (c.out.d_round_prims) c.out.d_round_prims[r0 + q] = (int)(wv >> 8);
+                run += (int)(wv & 0xFFu);
+            }
+        }
+        const unsigned long long my_src = (unsigned long long)suid;
+        const int ex = inc_u - my_u;
+        const int tot = __shfl_sync(0xffffffffu, inc_u, 31);
+        const bool want_uid = c.out.d_unique_ids != nullptr;
+        const bool want_pos = sp.kind == VR_SHADER_POSITION;
+        const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
+        const bool want_cnt = c.out.d_shade_counts != nullptr;
+        uint32_t* __restrict__ out_uid = c.out.d_unique_ids + off.y;
+        float4* __restrict__ shaded = reinterpret_cast<float4*>(c.out.d_shaded4) + off.y;
+        const uint32_t lt = (1u << lane) - 1;
+        int first_owner = 0;
+        constexpr int U4 = 4;
+        for (int j0 = 0; j0 < tot; j0 += 32 * U4) {
+            uint32_t uid[U4];
+            float4 pv[U4];
+#pragma unroll
+            for (int u = 0; u < U4; u++) {
+                const int jb = j0 + 32 * u;
+                const int d = inc_u - jb - 1;
+                const uint32_t ends = __reduce_or_sync(0xffffffffu, (my_u > 0 && d >= 0 && d < 32) ? (1u << d) : 0u);
+                const int owner = (first_owner + __popc(ends & lt)) & 31;
+                first_owner += __popc(ends);
+                const int oex = __shfl_sync(0xffffffffu, ex, owner);
+                const uint32_t* osrc = (const uint32_t*)__shfl_sync(0xffffffffu, my_src, owner);
+                const int j = jb + lane;
+                uid[u] = j < tot ? osrc[j - oex] : 0u;
+            }
+            if (want_pos) {
+#pragma unroll
+                for (int u = 0; u < U4; u++)
+                    if (j0 + 32 * u + lane < tot) pv[u] = __ldg(sp.pos4 + uid[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U4; u++) {
+                const int j = j0 + 32 * u + lane;
+                if (j >= tot) continue;
+                if (want_uid) out_uid[j] = uid[u];
+                if (want_pos) shaded[j] = transform_position(sp, pv[u]);
+                if (want_attr)
+                    for (int q = 0; q < sp.attr_words; q++)
+                        c.out.d_shaded_attr[((int64_t)off.y + j) * sp.attr_words + q] = __ldg(sp.attr + (int64_t)uid[u] * sp.attr_words + q);
+                if (want_cnt) atomicAdd(&c.out.d_shade_counts[uid[u]], 1);
+            }
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -729,32 +893,6 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
 // does it all; beyond that, 1024-segment tiles are reduced, the tile sums scanned by the
 // same single-CTA kernel, and a down-sweep writes the per-segment offsets.
 // ---------------------------------------------------------------------------------
-__device__ void finish_stats(const RunCtx& c, long long R, long long U) {
-    int64_t* st = c.out.d_stats;
-    for (int i = 0; i < VR_STATS_WORDS; i++) st[i] = 0;
-    long long span_total = 0;
-    if (c.n_batches > 0)
-        span_total = c.contiguous ? (long long)c.bend[c.n_batches - 1] - c.bbegin[0] : c.map_off[c.n_batches];
-    if (span_total > c.span_cap) report_error(c, 0, VR_ERR_CAPACITY);
-    if (U > c.out.cap_unique || R > c.out.cap_rounds || U > 0x7fffffffLL) report_error(c, 0, VR_ERR_CAPACITY);
-    st[VR_STAT_INDICES] = span_total;
-    st[VR_STAT_INVOCATIONS] = U;
-    st[VR_STAT_BATCHES] = c.n_batches;
-    st[VR_STAT_ROUNDS] = R;
-    st[VR_STAT_PROBES_FAST] = c.acc[ACC_PROBES_FAST];
-    st[VR_STAT_PROBES_SLOW] = c.acc[ACC_PROBES_SLOW];
-    st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
-    const long long e = c.acc[ACC_ERROR];
-    if (e == 0) {
-        st[VR_STAT_ERROR] = -1;
-        if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
-        if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
-    } else {
-        st[VR_STAT_ERROR] = ((0x7FFFFFFFFFFFLL - (e >> 8)) << 8) | (e & 0xFF);
-        c.acc[ACC_ABORT] = 1;  // K3 must not touch the outputs
-    }
-}
-
 __global__ void __launch_bounds__(1024) scan_block_kernel(RunCtx c, const int2* __restrict__ in, int2* __restrict__ out, int n) {
     __shared__ long long wr[32], wu[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -1040,7 +1178,7 @@ __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-    size_t map_off, counts, seg_counts, seg_off, tile_sums, tile_off, acc, stage_uid, stage_round, total;
+    size_t map_off, counts, seg_counts, seg_off, tile_sums, tile_off, acc, tile_state, stage_uid, stage_round, total;
     int stage_factor, seg_batches, n_segs, n_scan_tiles;
 };
 
@@ -1061,6 +1199,7 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.tile_sums = o; o += align_up((size_t)(L.n_scan_tiles + 1) * 8);
     L.tile_off = o; o += align_up((size_t)(L.n_scan_tiles + 2) * 8);
     L.acc = o; o += align_up(ACC_WORDS * 8);
+    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, kFastThreads) + 1) * 8);
     L.stage_uid = o;
     if (strategy != VR_NAIVE) o += align_up(((size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64) * 4);
     L.stage_round = o;
@@ -1074,6 +1213,7 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
 // vr_run is not re-entrant.
 static cudaEvent_t g_prof_ev[VR_PROFILE_STAGES + 1];
 static int g_prof_on = 0, g_prof_marks = 0;
+static int g_last_launches = 0;  // kernels launched by the last vr_run of this process
 static inline void prof_mark(cudaStream_t s) {
     if (g_prof_on && g_prof_marks <= VR_PROFILE_STAGES) cudaEventRecord(g_prof_ev[g_prof_marks++], s);
 }
@@ -1088,11 +1228,18 @@ static int launch_warp_tpb(const RunCtx& c, cudaStream_t stream) {
 }
 
 template <int W>
-static int launch_warp_fast(const RunCtx& c, int bs, cudaStream_t stream) {
+static int launch_warp_fast(const RunCtx& c, int bs, bool fused, const ShaderParams& sp, cudaStream_t stream) {
     const size_t smem = (size_t)kFastThreads * (64 + 4 * W + 2 * W);
-    if (smem > 48 * 1024)
-        VR_CUDA_CHECK(cudaFuncSetAttribute(warp_fast_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    warp_fast_kernel<W><<<(int)ceil_div(c.n_batches, kFastThreads), kFastThreads, smem, stream>>>(c, bs);
+    const int blocks = (int)ceil_div(c.n_batches, kFastThreads);
+    if (fused) {
+        if (smem > 48 * 1024)
+            VR_CUDA_CHECK(cudaFuncSetAttribute(warp_fast_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        warp_fast_kernel<W, true><<<blocks, kFastThreads, smem, stream>>>(c, bs, sp);
+    } else {
+        if (smem > 48 * 1024)
+            VR_CUDA_CHECK(cudaFuncSetAttribute(warp_fast_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        warp_fast_kernel<W, false><<<blocks, kFastThreads, smem, stream>>>(c, bs, sp);
+    }
     return VR_OK;
 }
 
@@ -1223,6 +1370,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
            const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_) {
     const bool no_budget = (strategy & VR_FLAG_NO_BUDGET) != 0;
     const bool static_batches = (strategy & VR_FLAG_STATIC) != 0;
+    const bool allow_fuse = (strategy & VR_FLAG_NO_FUSE) == 0;
     const bool contiguous = (strategy & VR_FLAG_CONTIGUOUS) != 0 || static_batches;
     strategy &= 0xFF;
     if (strategy < VR_NAIVE || strategy > VR_PHASH) return VR_ERR_UNKNOWN_STRATEGY;  // strategies.py:422-423
@@ -1268,6 +1416,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     c.tile_sums = (int2*)(ws + L.tile_sums);
     c.tile_off = (int2*)(ws + L.tile_off);
     c.acc = (long long*)(ws + L.acc);
+    c.tile_state = (unsigned long long*)(ws + L.tile_state);
     c.stage_uid = (uint32_t*)(ws + L.stage_uid);
     c.stage_round = (uint32_t*)(ws + L.stage_round);
     c.out = *out;
@@ -1296,22 +1445,25 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         VR_CUDA_CHECK(cudaFuncSetAttribute(hash_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
 
+    const bool fast_warp = strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0 && nb > 0;
+    const bool fused = fast_warp && allow_fuse;
+    c.n_fused_tiles = fused ? (int)ceil_div(nb, kFastThreads) : 0;
     g_prof_marks = 0;
     prof_mark(stream);
-    init_kernel<<<1, 32, 0, stream>>>(c);
+    init_kernel<<<(int)ceil_div(c.n_fused_tiles + ACC_WORDS, 256), 256, 0, stream>>>(c);
     if (!contiguous && nb > 0) span_scan_kernel<<<1, 1024, 0, stream>>>(c);
     prof_mark(stream);
     if (nb > 0) {
         if (strategy == VR_NAIVE) {
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
-        } else if (strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0) {
+        } else if (fast_warp) {
             const int bs = cfg->batch_size;
             switch (cfg->warp_width) {
-            case 4: st = launch_warp_fast<4>(c, bs, stream); break;
-            case 8: st = launch_warp_fast<8>(c, bs, stream); break;
-            case 16: st = launch_warp_fast<16>(c, bs, stream); break;
-            case 32: st = launch_warp_fast<32>(c, bs, stream); break;
-            default: st = launch_warp_fast<64>(c, bs, stream); break;
+            case 4: st = launch_warp_fast<4>(c, bs, fused, sp, stream); break;
+            case 8: st = launch_warp_fast<8>(c, bs, fused, sp, stream); break;
+            case 16: st = launch_warp_fast<16>(c, bs, fused, sp, stream); break;
+            case 32: st = launch_warp_fast<32>(c, bs, fused, sp, stream); break;
+            default: st = launch_warp_fast<64>(c, bs, fused, sp, stream); break;
             }
             if (st) return st;
         } else if (strategy == VR_WARP) {
@@ -1330,6 +1482,13 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         }
     }
     prof_mark(stream);
+    if (fused) {
+        prof_mark(stream);
+        prof_mark(stream);
+        g_last_launches = 2;
+        VR_CUDA_CHECK(cudaGetLastError());
+        return VR_OK;
+    }
     if (L.n_scan_tiles == 0) {
         scan_block_kernel<<<1, 1024, 0, stream>>>(c, c.seg_counts, c.seg_off, c.n_segs);
     } else {
@@ -1347,9 +1506,12 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         }
     }
     prof_mark(stream);
+    g_last_launches = (nb > 0 ? 3 : 1) + ((!contiguous && nb > 0) ? 1 : 0) + (L.n_scan_tiles ? 3 : 1);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
 }
+
+int vr_last_launch_count(void) { return g_last_launches; }
 
 int vr_expand_stream(const int32_t* d_bro, const int32_t* d_ruo, const int32_t* d_rprims, const uint16_t* d_amap,
                      const uint32_t* d_uids, const float* d_shaded4, int64_t nb, const int32_t* d_bbegin,

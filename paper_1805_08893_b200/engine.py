@@ -254,7 +254,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                n_batches: int, span_total: int, max_span: int, cfg: BatchConfig, hcfg=None,
                shader: ShaderSpec | None = None, *, want_counts: bool = False,
                buffers: RunBuffers | None = None, enforce_budget: bool = True,
-               contiguous: bool | None = None, static: bool = False) -> DeviceRun:
+               contiguous: bool | None = None, static: bool = False, fuse: bool = True) -> DeviceRun:
     """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back."""
     lib = N.require_cuda()
     if strategy not in N.STRATEGY_IDS:
@@ -265,7 +265,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         contiguous = (n_batches > 0 and d_begin.data_ptr() + 4 == d_end.data_ptr()
                       and d_begin.is_contiguous() and d_end.is_contiguous())
     flags = ((0 if enforce_budget else N.VR_FLAG_NO_BUDGET) | (N.VR_FLAG_CONTIGUOUS if contiguous else 0)
-             | (N.VR_FLAG_STATIC if static else 0))
+             | (N.VR_FLAG_STATIC if static else 0) | (0 if fuse else N.VR_FLAG_NO_FUSE))
     shader = shader or ShaderSpec()
     buffers = buffers or RunBuffers()
     c = _cfg_c(cfg)

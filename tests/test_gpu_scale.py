@@ -7,7 +7,7 @@ import pytest
 
 import oracle as O
 import paper_1805_08893_b200 as P
-from helpers import assert_flat_equal, oracle_flat
+from helpers import MATRIX, assert_flat_equal, oracle_flat
 from paper_1805_08893_b200 import _native as N
 from paper_1805_08893_b200 import engine
 from paper_1805_08893_b200.batching import BatchConfig
@@ -23,30 +23,58 @@ def dragon_grid():
     return mesh
 
 
-def test_config3_warp(cuda_lib, dragon_grid):
-    """224 914 batches, 449 827 rounds, 8 100 190 invocations."""
+WARP_PATHS = {"generic": dict(), "static": dict(static=True, fuse=False), "fused": dict(static=True)}
+
+
+@pytest.mark.parametrize("path", sorted(WARP_PATHS))
+def test_config3_warp(cuda_lib, dragon_grid, path):
+    """224 914 batches, 449 827 rounds, 8 100 190 invocations -- through the
+    generic thread-per-batch kernel, the static-batch kernel and the fused kernel."""
+    import torch
     mesh = dragon_grid
     cfg = BatchConfig()
+    kw = WARP_PATHS[path]
     d_idx = engine.to_device_indices(mesh.indices)
     offs = engine.static_offsets_device(len(mesh.indices), cfg)
     nb = offs.numel() - 1
     spec = engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY, vertex_count=mesh.vertex_count)
     run = engine.run_device("warp", d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 96, cfg, None, spec,
-                            want_counts=True).check()
+                            want_counts=True, **kw).check()
     assert (nb, run.rounds, run.invocations) == (224914, 449827, 8100190)
     assert abs(1 - run.invocations / run.indices - 0.624846) < 1e-6
     assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
     assert int(run.shade_counts.sum().item()) == run.invocations
     # bit-exact against the oracle on a prefix and on a window in the middle of the stream
     for lo in (0, 3000 * 96 * 30):
-        sub = mesh.indices[lo:lo + 96 * 3000]
+        sub = mesh.indices[lo:lo + 96 * 3000 + 33]  # ragged last batch
         so = O.static_batches(len(sub))
         fr = O.run("warp", sub, so[:-1], so[1:])
-        import torch
         o = torch.from_numpy(so.astype(np.int32)).cuda()
         r = engine.run_device("warp", engine.to_device_indices(sub), o[:-1], o[1:], len(so) - 1, len(sub), 96,
-                              cfg, None, engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
-        assert_flat_equal(r.flat(), oracle_flat(fr), f"window {lo}")
+                              cfg, None, engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY), **kw)
+        assert_flat_equal(r.flat(), oracle_flat(fr), f"{path} window {lo}")
+
+
+@pytest.mark.parametrize("width", [4, 8, 16, 32, 64])
+def test_warp_paths_agree_all_widths(cuda_lib, width):
+    """Static-batch and fused kernels against the oracle for every warp width, positions shaded."""
+    import torch
+    mesh = P.shuffle_triangles(P.gen_grid(90, 70), 3) if width in (8, 32) else P.gen_grid(90, 70)
+    for bs in (96, 24, 192):
+        cfg = BatchConfig(batch_size=bs, warp_width=width)
+        so = O.static_batches(len(mesh.indices), batch_size=bs)
+        fr = O.run("warp", mesh.indices, so[:-1], so[1:], warp_width=width)
+        want = O.shade_positions(mesh.positions, fr.unique_ids, MATRIX)
+        o = torch.from_numpy(so.astype(np.int32)).cuda()
+        for path, kw in WARP_PATHS.items():
+            spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                                     matrix=MATRIX, vertex_count=mesh.vertex_count)
+            r = engine.run_device("warp", engine.to_device_indices(mesh.indices), o[:-1], o[1:], len(so) - 1,
+                                  len(mesh.indices), bs, cfg, None, spec, want_counts=True, **kw)
+            flat = r.flat()
+            assert_flat_equal(flat, oracle_flat(fr), f"w={width} bs={bs} {path}")
+            np.testing.assert_allclose(flat["shaded"][:, :3], want, rtol=1e-5, atol=1e-5)
+            assert np.array_equal(flat["shade_counts"], O.shade_counts(fr.unique_ids, mesh.vertex_count))
 
 
 def test_config3_mesh_dynamic_sort(cuda_lib, dragon_grid):
