@@ -853,11 +853,14 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
         }
     }
     __syncthreads();
-    // phase 3
+    // phase 3: no walking -- the final slot of every first occurrence is read off the table
+    // (slot_of[position] = slot), duplicates take the slot of their first occurrence, and the
+    // probe chain of the reference's loop is the circular distance from the home slot + 1.
     for (int s = tid; s < (int)tsize; s += nt) {
         uint32_t p = tpos[s];
         tid_[s] = p == kEmpty ? kEmpty : ids[p];
         occ[s] = p != kEmpty;
+        if (p != kEmpty) kpos[maps[p]] = (uint32_t)s;  // private-set slot of this id -> table slot
     }
     __syncthreads();
     block_exclusive_scan(occ, (int)tsize, scratch);
@@ -867,10 +870,9 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
     unsigned int csum = 0;
     int cmax = 0;
     for (int i = tid; i < n; i += nt) {
-        uint32_t id = ids[i];
-        uint32_t h0 = hash_slot(id, c.multiplier, c.table_bits), s = h0;
-        while (tid_[s] != id) s = (s + 1) & tmask;
-        int chain = (int)((s - h0) & tmask) + 1;
+        const uint32_t s = kpos[maps[i]];
+        const uint32_t h0 = hash_slot(ids[i], c.multiplier, c.table_bits);
+        const int chain = (int)((s - h0) & tmask) + 1;
         csum += chain;
         cmax = max(cmax, chain);
         maps[i] = (uint16_t)occ[s];
@@ -884,6 +886,160 @@ __global__ void __launch_bounds__(256) hash_batch_kernel(RunCtx c, int nmax, int
         c.counts[b] = make_int2(1, nu);
         atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], s_chain_sum);
         atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)s_chain_max);
+        if (c.enforce_budget && nu > c.max_unique) report_error(c, b, VR_ERR_OVER_BUDGET);
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// K1 (hash), one WARP per batch: same three phases as hash_batch_kernel, sized for the dynamic
+// batches of the paper (<= 1023 indices, <= 256 unique ids): 8 batches per 256-thread CTA, no
+// CTA barriers, lanes stride the batch.  The private first-occurrence set is sized by the
+// unique budget (2x, power of two), not by the batch length.
+// ---------------------------------------------------------------------------------
+struct HashWarpSmem { int n_max, q, per_warp_bytes; };
+
+__global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int q, int u_bound, int per_warp_bytes) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int warps = blockDim.x >> 5;
+    const int b = blockIdx.x * warps + wid;
+    if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
+    unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
+    uint32_t* ids = reinterpret_cast<uint32_t*>(base);
+    uint32_t* kkey = ids + n_max;
+    uint32_t* kpos = kkey + q;
+    uint32_t* tpos = kpos + q;
+    uint16_t* rank_of = reinterpret_cast<uint16_t*>(tpos + c.table_size);
+    uint16_t* kslot = rank_of + c.table_size;
+    int begin, n;
+    if (!validate_batch(c, b, begin, n)) {
+        if (lane == 0) c.counts[b] = make_int2(0, 0);
+        return;
+    }
+    const int mo = batch_map_off(c, b, begin);
+    const uint32_t tsize = c.table_size, tmask = tsize - 1;
+    const uint32_t qmask = (uint32_t)q - 1;
+    const int qbits = ilog2((uint32_t)q);
+    for (int i = lane; i < n; i += 32) ids[i] = __ldg(c.idx + begin + i);
+    for (int i = lane; i < q; i += 32) { kkey[i] = kEmpty; kpos[i] = kEmpty; }
+    for (int i = lane; i < (int)tsize; i += 32) tpos[i] = kEmpty;
+    __syncwarp();
+    // phase 1: first occurrences.  The set holds at most u_bound + 32 distinct ids.
+    int fresh = 0;
+    bool overflow = false;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < n && !overflow) {
+            const uint32_t id = ids[i];
+            uint32_t h = (id * 0x9E3779B1u) >> (32 - qbits);
+            for (;;) {
+                const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
+                if (prev == kEmpty) fresh++;
+                if (prev == kEmpty || prev == id) break;
+                h = (h + 1) & qmask;
+            }
+            atomicMin(&kpos[h], (uint32_t)i);
+            kslot[i] = (uint16_t)h;
+        }
+        int tot = fresh;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+        overflow = tot > u_bound;  // uniform: stop before the set can fill up
+        if (overflow) break;
+    }
+    int nu = fresh;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) nu += __shfl_xor_sync(0xffffffffu, nu, d);
+    if (overflow || nu > (int)tsize) {
+        // more unique ids than table slots: the reference's chain would exceed table_size (strategies.py:283-284)
+        if (lane == 0) {
+            report_error(c, b, VR_ERR_HASH_FULL);
+            c.counts[b] = make_int2(0, 0);
+        }
+        return;
+    }
+    __syncwarp();
+    // phase 2: first occurrences enter the reference table in WAVES of 32, in position order.
+    // When a wave starts every earlier first occurrence sits in its final slot, so the wave's
+    // elements jump over those slots with a find-next-zero on an occupancy bitmap (that is what
+    // the reference's probe loop does one slot at a time) and only compete among themselves:
+    // atomicMin with displacement, the earlier position wins the slot (strategies.py:277-294).
+    uint32_t* bitmap = reinterpret_cast<uint32_t*>(kslot + n_max);  // [max(1, tsize/32)] occupied slots
+    const int n_words = tsize >= 32 ? (int)(tsize >> 5) : 1;
+    for (int w = lane; w < n_words; w += 32) bitmap[w] = (tsize >= 32) ? 0u : ~((1u << tsize) - 1u);
+    // list of first-occurrence positions, ascending (kept in rank_of until phase 3 rewrites it)
+    {
+        int run = 0;
+        for (int i0 = 0; i0 < n; i0 += 32) {
+            const int i = i0 + lane;
+            const bool f = i < n && kpos[kslot[i]] == (uint32_t)i;
+            const uint32_t m = __ballot_sync(0xffffffffu, f);
+            if (f) rank_of[run + __popc(m & ((1u << lane) - 1))] = (uint16_t)i;
+            run += __popc(m);
+        }
+    }
+    __syncwarp();
+    for (int w0 = 0; w0 < nu; w0 += 32) {
+        uint32_t cur = (w0 + lane < nu) ? (uint32_t)rank_of[w0 + lane] : kEmpty;
+        uint32_t h = cur != kEmpty ? hash_slot(ids[cur], c.multiplier, c.table_bits) : 0u;
+        uint32_t taken = kEmpty;  // slot this lane turned from empty to occupied
+        while (__any_sync(0xffffffffu, cur != kEmpty)) {
+            if (cur != kEmpty) {
+                // next slot at or after h that no earlier wave occupies
+                uint32_t wi = h >> 5;
+                uint32_t bits = ~bitmap[wi] & (0xFFFFFFFFu << (h & 31));
+                while (bits == 0) { wi = (wi + 1) & (uint32_t)(n_words - 1); bits = ~bitmap[wi]; }
+                const uint32_t sl = (wi << 5) + (uint32_t)__ffs((int)bits) - 1;
+                const uint32_t old = atomicMin(&tpos[sl], cur);
+                if (old == kEmpty) {
+                    taken = sl;  // a lane takes at most one empty slot per wave
+                    cur = kEmpty;
+                } else {
+                    if (old > cur) cur = old;  // displaced a later insertion of this wave: carry it on
+                    h = (sl + 1) & tmask;
+                }
+            }
+        }
+        __syncwarp();
+        if (taken != kEmpty) atomicOr(&bitmap[taken >> 5], 1u << (taken & 31));
+        __syncwarp();
+    }
+    // phase 3: ranks in table order, unique ids, slot of every id
+    uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
+    int run = 0;
+    for (int s0 = 0; s0 < (int)tsize; s0 += 32) {
+        const int s = s0 + lane;
+        const uint32_t p = s < (int)tsize ? tpos[s] : kEmpty;
+        const uint32_t occ = __ballot_sync(0xffffffffu, p != kEmpty);
+        if (p != kEmpty) {
+            const int rk = run + __popc(occ & ((1u << lane) - 1));
+            rank_of[s] = (uint16_t)rk;
+            suid[rk] = ids[p];
+            kpos[kslot[p]] = (uint32_t)s;
+        }
+        run += __popc(occ);
+    }
+    __syncwarp();
+    unsigned int csum = 0;
+    int cmax = 0;
+    uint16_t* __restrict__ amap = c.out.d_assembly_map ? c.out.d_assembly_map + mo : nullptr;
+    for (int i = lane; i < n; i += 32) {
+        const uint32_t s = kpos[kslot[i]];
+        const uint32_t h0 = hash_slot(ids[i], c.multiplier, c.table_bits);
+        const int chain = (int)((s - h0) & tmask) + 1;
+        csum += chain;
+        cmax = max(cmax, chain);
+        if (amap) amap[i] = rank_of[s];
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        csum += __shfl_xor_sync(0xffffffffu, csum, d);
+        cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, d));
+    }
+    if (lane == 0) {
+        c.counts[b] = make_int2(1, nu);
+        atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], (unsigned long long)csum);
+        atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)cmax);
         if (c.enforce_budget && nu > c.max_unique) report_error(c, b, VR_ERR_OVER_BUDGET);
     }
 }
@@ -1478,7 +1634,20 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         } else if (strategy == VR_SORT) {
             sort_batch_kernel<<<nbi, 256, smem, stream>>>(c, pmax);
         } else {
-            hash_batch_kernel<<<nbi, 256, smem, stream>>>(c, nmax, q);
+            // one warp per batch when a warp's tables fit comfortably; else one CTA per batch
+            const int u_bound = (uint32_t)max_span < hc.table_size ? max_span : (int)hc.table_size;
+            const int wn = (max_span + 31) & ~31;
+            const int wq = (int)next_pow2((uint32_t)(2 * (u_bound + 1) + 64));
+            const int per_warp = (wn * 4 + wq * 8 + (int)hc.table_size * 6 + wn * 2 + ((int)hc.table_size >> 3) + 4 + 15) & ~15;
+            if (per_warp <= 24 * 1024 && hc.table_size <= 4096) {
+                int warps = 8;
+                while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
+                const size_t wsmem = (size_t)warps * per_warp;
+                VR_CUDA_CHECK(cudaFuncSetAttribute(hash_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+                hash_warp_kernel<<<(int)ceil_div(nb, warps), warps * 32, wsmem, stream>>>(c, wn, wq, u_bound, per_warp);
+            } else {
+                hash_batch_kernel<<<nbi, 256, smem, stream>>>(c, nmax, q);
+            }
         }
     }
     prof_mark(stream);
