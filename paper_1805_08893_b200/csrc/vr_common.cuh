@@ -84,15 +84,16 @@ struct ShaderParams {
     int vertex_count;
 };
 
-// The w-divide uses one reciprocal (MUFU.RCP + Newton step, <= 1 ulp) and three multiplies:
-// <= 2 ulp of FP32 from the reference's float64 result, far inside the 1e-5 relative bound.
+// The w-divide uses one hardware reciprocal (MUFU.RCP, <= 1 ulp) and three multiplies: a few ulp
+// of FP32 from the reference's float64 result, far inside the 1e-5 relative bound.
 __device__ __forceinline__ float4 transform_position(const ShaderParams& sp, float4 p) {
     if (!sp.has_matrix) return make_float4(p.x, p.y, p.z, 1.0f);
     const float ox = fmaf(sp.m[0], p.x, fmaf(sp.m[1], p.y, fmaf(sp.m[2], p.z, sp.m[3])));
     const float oy = fmaf(sp.m[4], p.x, fmaf(sp.m[5], p.y, fmaf(sp.m[6], p.z, sp.m[7])));
     const float oz = fmaf(sp.m[8], p.x, fmaf(sp.m[9], p.y, fmaf(sp.m[10], p.z, sp.m[11])));
     const float ow = fmaf(sp.m[12], p.x, fmaf(sp.m[13], p.y, fmaf(sp.m[14], p.z, sp.m[15])));
-    const float iw = __frcp_rn(ow);
+    float iw;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(iw) : "f"(ow));
     return make_float4(ox * iw, oy * iw, oz * iw, ow);
 }
 

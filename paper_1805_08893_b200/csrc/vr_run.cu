@@ -703,6 +703,8 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
     }
 }
 
+#include "vr_warp_rows.cuh"
+
 // ---------------------------------------------------------------------------------
 // K1 (sort): strategies.py:235-260 -- Algorithm 2.  One CTA per batch: bitonic sort of
 // (id << 32 | slot) keys in shared memory (the slot in the low half makes it the stable
@@ -1355,7 +1357,7 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.tile_sums = o; o += align_up((size_t)(L.n_scan_tiles + 1) * 8);
     L.tile_off = o; o += align_up((size_t)(L.n_scan_tiles + 2) * 8);
     L.acc = o; o += align_up(ACC_WORDS * 8);
-    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, kFastThreads) + 1) * 8);
+    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 64) + 1) * 8);  // kRowThreads tiles (>= kFastThreads tiles)
     L.stage_uid = o;
     if (strategy != VR_NAIVE) o += align_up(((size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64) * 4);
     L.stage_round = o;
@@ -1603,7 +1605,11 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
 
     const bool fast_warp = strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0 && nb > 0;
     const bool fused = fast_warp && allow_fuse;
-    c.n_fused_tiles = fused ? (int)ceil_div(nb, kFastThreads) : 0;
+    // tile kernel (vr_warp_rows.cuh) when a batch row fits shared memory comfortably
+    RowsGeom rg{};
+    const bool rows = fused && rows_geometry(cfg->warp_width, cfg->batch_size, rg) &&
+                      (((uintptr_t)out->d_assembly_map) & 15) == 0;
+    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : 0;
     g_prof_marks = 0;
     prof_mark(stream);
     init_kernel<<<(int)ceil_div(c.n_fused_tiles + ACC_WORDS, 256), 256, 0, stream>>>(c);
@@ -1612,6 +1618,16 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (nb > 0) {
         if (strategy == VR_NAIVE) {
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
+        } else if (rows) {
+            const int bs = cfg->batch_size;
+            switch (cfg->warp_width) {
+            case 4: st = launch_warp_rows<4>(c, bs, rg, sp, stream); break;
+            case 8: st = launch_warp_rows<8>(c, bs, rg, sp, stream); break;
+            case 16: st = launch_warp_rows<16>(c, bs, rg, sp, stream); break;
+            case 32: st = launch_warp_rows<32>(c, bs, rg, sp, stream); break;
+            default: st = launch_warp_rows<64>(c, bs, rg, sp, stream); break;
+            }
+            if (st) return st;
         } else if (fast_warp) {
             const int bs = cfg->batch_size;
             switch (cfg->warp_width) {
@@ -1681,6 +1697,16 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
 }
 
 int vr_last_launch_count(void) { return g_last_launches; }
+
+#ifdef VR_TIMELINE
+// debugging aid (not part of the ABI): copies the phase time stamps of the last tile-kernel launch
+int vr_debug_timeline(unsigned long long* host, int cap) {
+    const int n = kTimelineMarks * 2 * kTimelineTiles;
+    if (cap < n) return -n;
+    if (cudaMemcpyFromSymbol(host, g_timeline, sizeof(unsigned long long) * n) != cudaSuccess) return 0;
+    return n;
+}
+#endif
 
 int vr_expand_stream(const int32_t* d_bro, const int32_t* d_ruo, const int32_t* d_rprims, const uint16_t* d_amap,
                      const uint32_t* d_uids, const float* d_shaded4, int64_t nb, const int32_t* d_bbegin,
