@@ -1607,8 +1607,10 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     const bool fused = fast_warp && allow_fuse;
     // tile kernel (vr_warp_rows.cuh) when a batch row fits shared memory comfortably
     RowsGeom rg{};
+    // (its packed table entries hold 24-bit ids: the caller must state a vertex count that fits)
     const bool rows = fused && rows_geometry(cfg->warp_width, cfg->batch_size, rg) &&
-                      (((uintptr_t)out->d_assembly_map) & 15) == 0;
+                      (((uintptr_t)out->d_assembly_map) & 15) == 0 && shader && shader->vertex_count > 0 &&
+                      shader->vertex_count <= (1 << 24);
     c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : 0;
     g_prof_marks = 0;
     prof_mark(stream);
