@@ -307,7 +307,7 @@ def main():
         peak, peak_src = (peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)") if "hbm_gbs" in peaks \
             else (6650.0, "fallback (B200_PROFILING.md)")
         launches = lib.vr_last_launch_count()
-        fused = launches == 2  # init + one kernel that dedups, places and shades
+        fused = launches in (2, 3)  # init + one kernel that dedups, places and shades (+ its drain kernel)
         dom = int(np.argmax(stage_ms))
         # per-kernel algorithmic bytes: dedup = index read + map write + metadata;
         # shade/finalize = staged id read is not algorithmic: position read + shaded write

@@ -1359,7 +1359,14 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.acc = o; o += align_up(ACC_WORDS * 8);
     L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 64) + 1) * 8);  // kRowThreads tiles (>= kFastThreads tiles)
     L.stage_uid = o;
-    if (strategy != VR_NAIVE) o += align_up(((size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64) * 4);
+    if (strategy != VR_NAIVE) {
+        size_t words = (size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64;
+        if (strategy == VR_WARP) {  // the tile kernel keeps its claim lists here (vr_warp_rows.cuh)
+            const size_t tw = rows_scratch_words(w, cfg->batch_size, nb);
+            if (tw > words) words = tw;
+        }
+        o += align_up(words * 4);
+    }
     L.stage_round = o;
     if (strategy == VR_WARP) o += align_up(((size_t)span_total / ps + nb + 64) * 4);
     L.total = o;
@@ -1672,7 +1679,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (fused) {
         prof_mark(stream);
         prof_mark(stream);
-        g_last_launches = 2;
+        g_last_launches = rows ? 3 : 2;  // init + tile kernel (+ drain kernel)
         VR_CUDA_CHECK(cudaGetLastError());
         return VR_OK;
     }

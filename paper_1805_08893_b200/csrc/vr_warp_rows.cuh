@@ -1,29 +1,33 @@
 // vr_warp_rows.cuh -- warp voting (strategies.py:173-232) for static batches, tile kernel.
 // Included by vr_run.cu inside namespace vr (uses RunCtx, report_error, finish_stats, lds_*/sts_*).
 //
-// One CTA owns a TILE of 64 consecutive static batches (batching.py:76-84), i.e. one contiguous
-// 64 * batch_size * 4-byte piece of the index buffer, and takes it through the whole stage.  The
-// CTA has 2 dedup warps (one thread per batch) and 4 helper warps: shared memory, not registers,
-// limits the tiles in flight per SM, so the helpers are free parallelism for every phase that is
-// not the per-batch dedup chain (look-back, local-index write-out, claim compaction, shading).
+// A TILE is 64 consecutive static batches (batching.py:76-84): one contiguous 64 * batch_size *
+// 4-byte piece of the index buffer.  A CTA has 2 dedup warps (one thread per batch) and 4 helper
+// warps, and works on TWO tiles at once -- software pipelining across tiles:
 //
-//   A  stage    every dedup thread issues ONE bulk asynchronous copy (cp.async.bulk, the 1-D TMA
-//               path, completion on an mbarrier) of its batch's indices into its own shared-memory
-//               ROW.  The tile is read from HBM as whole 128-byte lines, no register staging.
-//   B  dedup    one THREAD per batch runs the closed form of Algorithm 1 over its row as a per-lane
-//               state machine (see below): claimed ids of the current round live in a private
-//               open-addressing table entry[slot][thread]; claims are appended IN PLACE at the
-//               front of the row (a claim never overtakes the read cursor: claims so far <= slots
-//               read + 2 per finished round, and the row starts with that much slack), so the
-//               unique ids never leave the SM before they are shaded; local indices are bytes in
-//               a rank row.
-//   C  place    the CTA's (rounds, ids) aggregate enters a decoupled look-back over tiles (ticket
-//               order) run by one helper warp, while the other warps write the local indices as
-//               coalesced 16-byte stores (8 x uint16) and compact the rows' claims into one flat
-//               list (in the table's shared memory, which is dead by then);
-//   D  shade    all 6 warps stream the flat list: coalesced id store, 16-byte position gather
-//               (prefetched into L2 when the id was claimed), FP32 4x4 transform + w-divide
-//               (strategies.py:53-67), coalesced 16-byte stores, 4 gathers in flight per thread.
+//   dedup warps, tile i (ticket order)
+//     A  stage   every row (batch) arrives by ONE bulk asynchronous copy (cp.async.bulk, the 1-D
+//                TMA path, completion on an mbarrier) into its own shared-memory row: the tile is
+//                read from HBM as whole 128-byte lines, no register staging.
+//     B  dedup   one THREAD per batch runs the closed form of Algorithm 1 over its row as a
+//                per-lane state machine (see below).  Claims are appended IN PLACE at the front of
+//                the row, local indices are bytes in a rank row.
+//     C  post    all six warps: local indices leave as coalesced 16-byte stores (8 x uint16); the
+//                rows' claims are copied, compacted, into the tile's slot of an L2-resident
+//                scratch list together with the per-row round records; then the tile's
+//                (rounds, claims) AGGREGATE is published and the CTA is done -- it never waits
+//                for its output offsets, its shared memory is free for the next tile.
+//   helper warps, tile j = i - K  (K = CTAs resident on the GPU: tile j is complete by then)
+//     D  offsets decoupled look-back over the published aggregates (no waiting in the steady
+//                state: every predecessor of j finished long ago); publishes j's inclusive prefix;
+//     E  shade   the tile's flat claim list is streamed from the scratch (L2 hits): coalesced id
+//                store, 16-byte position gather, FP32 4x4 transform + w-divide (strategies.py:53-67),
+//                coalesced 16-byte stores; round tables from the round records.
+//                This memory-bound work runs UNDER the compute-bound dedup of tile i.
+//     F  check   every index of tile i is range-checked against the vertex count and its vertex
+//                prefetched into L2 (it is gathered ~K tiles later).
+//
+// The last K tiles are shaded by a light second kernel (rows_drain_kernel).
 #pragma once
 
 constexpr int kRowThreads = 64;      // batches per tile = dedup threads
@@ -34,6 +38,10 @@ struct RowsGeom {
     int slack;       // words in front of the indices that absorb the tail re-claims
     int rk_stride;   // bytes per rank row (an odd number of words)
     int max_rounds;  // upper bound of rounds per batch
+    int row_cap;     // upper bound of claims per batch
+    int tile_words;  // scratch words per tile: meta[2][64] | rounds[64][max_rounds] | claims[64 * row_cap]
+    int lag;         // K: the helpers of the CTA with ticket i shade tile i - K
+    int n_tiles;
     uint32_t cpr_magic;  // ceil(2^32 / (batch_size / 8)): chunk -> row by multiply-high
     size_t smem;
 };
@@ -43,17 +51,24 @@ static inline bool rows_geometry(int W, int bs, RowsGeom& g) {
     if (bs % 24 != 0 || bs > 384) return false;  // whole 16-byte quads, whole 8-slot chunks
     const int per_round = 3 * (W / 3);
     g.max_rounds = (bs + per_round - 1) / per_round;
-    g.slack = (2 * (g.max_rounds - 1) + 3) & ~3;
+    g.slack = (2 * g.max_rounds + 2) & ~3;  // >= 2 * max_rounds - 1: see the claim-list store in the dedup loop
     int rw = bs + g.slack;
     while ((rw & 7) != 4) rw += 4;
     g.row_words = rw;
     g.rk_stride = bs + 4;  // odd number of words: same-slot byte stores of a warp are conflict-free
+    g.row_cap = bs + 2 * g.max_rounds;
+    g.tile_words = kRowThreads * (2 + g.max_rounds + g.row_cap);
     const int cpr = bs / 8;
     g.cpr_magic = (uint32_t)(((1ull << 32) + cpr - 1) / cpr);  // exact for chunk * cpr < 2^32
     const int S = 2 * W;
-    if (bs + 2 * g.max_rounds > S * kRowThreads) return false;  // one row's claims fit the flat list
     g.smem = (size_t)kRowThreads * ((size_t)rw * 4 + (size_t)S * 4 + (size_t)g.rk_stride + (size_t)g.max_rounds * 4 + 4);
     return g.smem <= 100 * 1024;
+}
+// scratch words needed by the tile kernel for nb batches (aliases the staging area of the other kernels)
+static inline size_t rows_scratch_words(int W, int bs, int64_t nb) {
+    RowsGeom g;
+    if (!rows_geometry(W, bs, g)) return 0;
+    return (size_t)ceil_div(nb, kRowThreads) * (size_t)g.tile_words;
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -78,10 +93,18 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
                  ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 #ifdef VR_TIMELINE
-// debugging aid: per-tile phase time stamps (ns, %globaltimer) of dedup warps 0/1; vr_debug_timeline() reads them
-constexpr int kTimelineMarks = 6, kTimelineTiles = 4096;
+// debugging aid: per-tile phase time stamps (ns, %globaltimer) of dedup warp 0 and helper warp 2
+constexpr int kTimelineMarks = 12, kTimelineTiles = 8192;
 __device__ unsigned long long g_timeline[kTimelineMarks * 2 * kTimelineTiles];
 __device__ __forceinline__ unsigned long long timeline_now() {
     unsigned long long v;
@@ -90,8 +113,8 @@ __device__ __forceinline__ unsigned long long timeline_now() {
 }
 #define VR_MARK_AT(k, value)                                                                   \
     do {                                                                                       \
-        if ((t & 31) == 0 && t < 64 && tile < kTimelineTiles)                                  \
-            g_timeline[((k) * 2 + (t >> 5)) * kTimelineTiles + tile] = (value);                \
+        if ((t & 31) == 0 && ((t >> 5) == 0 || (t >> 5) == 2) && tile < kTimelineTiles)        \
+            g_timeline[((k) * 2 + ((t >> 5) ? 1 : 0)) * kTimelineTiles + tile] = (value);      \
     } while (0)
 #define VR_MARK(k) VR_MARK_AT(k, timeline_now())
 #else
@@ -99,62 +122,235 @@ __device__ __forceinline__ unsigned long long timeline_now() {
 #define VR_MARK(k) do {} while (0)
 #endif
 
+// ---- D/E: shading of one finished tile by 128 threads (4 warps; `ht` = 0..127).  Used by the helper
+// warps of the tile kernel (tile = ticket - K) and by the drain kernel (the last K tiles).
+template <int DUMMY>
+__device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom& g, const ShaderParams& sp, int stile, int ht,
+                                                int2* s_base_ptr) {
+    constexpr int T = kRowThreads, NH = kRowCtaThreads - kRowThreads;
+    const int lane = ht & 31;
+    const bool lb_warp = ht < 32;
+    int2& s_base = *s_base_ptr;
+#ifdef VR_TIMELINE
+    const int t = ht + 64, tile = stile + g.lag;  // marks are filed under the CTA's own tile
+#endif
+    // Every helper warp waits for the tile's aggregate (normally published long ago: K tiles
+    // back) -- it carries the claim count, and acquiring it makes the tile's scratch visible.
+    unsigned long long mine = 0;
+    bool lost = false;
+    {
+        int spins = 0;
+        for (;;) {
+            if (lane == 0) mine = ld_relaxed_gpu_u64(c.tile_state + stile);
+            mine = __shfl_sync(0xffffffffu, mine, 0);
+            if (mine >> 62) break;
+            if (++spins > (1 << 22)) { lost = true; break; }
+        }
+        __threadfence();  // acquire
+    }
+    VR_MARK(8);
+    const int tot = lost ? 0 : (int)(mine & 0xFFFFFFFFull) ;
+    const uint32_t* __restrict__ sc = c.stage_uid + (size_t)stile * (size_t)g.tile_words;
+    const uint32_t* __restrict__ claims = sc + T * (2 + g.max_rounds);
+    const bool want_uid = c.out.d_unique_ids != nullptr;
+    const bool want_pos = sp.kind == VR_SHADER_POSITION;
+    uint32_t m0 = 0, m1 = 0;  // round-table metadata of row ht, in flight with everything else
+    if (ht < T) { m0 = __ldcg(sc + ht); m1 = __ldcg(sc + T + ht); }
+    // ---- E (part 1): the first U8 claims of every thread are gathered and shaded while the
+    // first helper warp is still resolving the tile's output offsets
+    constexpr int U8 = 8;
+    uint32_t uid[U8], nxt[U8];
+    float4 pv[U8];
+#pragma unroll
+    for (int u = 0; u < U8; u++) uid[u] = ht + NH * u < tot ? __ldcg(claims + ht + NH * u) : 0u;
+#pragma unroll
+    for (int u = 0; u < U8; u++) nxt[u] = ht + NH * (U8 + u) < tot ? __ldcg(claims + ht + NH * (U8 + u)) : 0u;
+    if (want_pos) {
+#pragma unroll
+        for (int u = 0; u < U8; u++)
+            if (ht + NH * u < tot) pv[u] = __ldg(sp.pos4 + uid[u]);
+#pragma unroll
+        for (int u = 0; u < U8; u++)  // the next step's vertices: on their way to L2 while this step is shaded
+            if (ht + NH * (U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
+    }
+    // ---- D: output offsets of tile stile by decoupled look-back (first helper warp)
+    if (lb_warp) {
+        const long long ar = (long long)((mine >> 32) & 0x3FFFFFFFull), au = (long long)(mine & 0xFFFFFFFFull);
+        // Each step inspects the 128 nearest predecessors (4 per lane, all loads in flight
+        // together); the walk ends at the nearest tile that already holds an inclusive prefix.
+        long long pr = 0, pu = 0;  // this lane's share of the exclusive prefix of the tile
+        bool found = false;
+        constexpr int LB = 4;
+        for (int pz = stile - 1; pz >= 0 && !found && !lost; pz -= 32 * LB) {
+            unsigned long long word[LB];
+            int spins = 0;
+            for (;;) {
+                bool pending = false;
+#pragma unroll
+                for (int k = 0; k < LB; k++) {
+                    const int idx = pz - lane - 32 * k;
+                    word[k] = ld_relaxed_gpu_u64(c.tile_state + (idx >= 0 ? idx : 0));
+                }
+#pragma unroll
+                for (int k = 0; k < LB; k++) {
+                    if (pz - lane - 32 * k < 0) word[k] = kStateInclusive + 0ull;  // before the first tile: inclusive zero
+                    pending |= (word[k] >> 62) == 0;
+                }
+                if (!__any_sync(0xffffffffu, pending)) break;
+                if (++spins > (1 << 22)) { lost = true; break; }
+            }
+            if (lost) break;
+#pragma unroll
+            for (int k = 0; k < LB; k++) {
+                const uint32_t incl = __ballot_sync(0xffffffffu, (word[k] >> 62) == 2);
+                const int upto = found ? -1 : (incl ? __ffs(incl) - 1 : 31);
+                if (lane <= upto) {
+                    pr += (long long)((word[k] >> 32) & 0x3FFFFFFFull);
+                    pu += (long long)(word[k] & 0xFFFFFFFFull);
+                }
+                found |= incl != 0;
+            }
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            pr += __shfl_xor_sync(0xffffffffu, pr, d);
+            pu += __shfl_xor_sync(0xffffffffu, pu, d);
+        }
+        const long long er = pr, eu = pu;
+        if (lane == 0) {
+            if (lost) report_error(c, (int64_t)stile * T, VR_ERR_CUDA);
+            const long long R = er + ar, U = eu + au;
+            st_relaxed_gpu_u64(c.tile_state + stile, kStateInclusive | ((unsigned long long)(R & 0x3FFFFFFF) << 32) | (unsigned long long)(U & 0xFFFFFFFFll));
+            const bool fits = U <= c.out.cap_unique && R <= c.out.cap_rounds && U <= 0x7fffffffLL && !lost;
+            if (!fits) report_error(c, (int64_t)stile * T, VR_ERR_CAPACITY);
+            s_base = fits ? make_int2((int)er, (int)eu) : make_int2(-1, -1);
+            if (stile == g.n_tiles - 1) { __threadfence(); finish_stats(c, R, U); }
+        }
+    }
+    VR_MARK(9);
+    asm volatile("bar.sync 1, %0;" ::"n"(NH) : "memory");  // helpers: offsets known
+    const int2 off = s_base;
+    if (off.x >= 0) {
+        // ---- E (part 2): stores; further claims U8 at a time, their ids loaded one step ahead
+        for (int j0 = ht;; j0 += NH * U8) {
+#pragma unroll
+            for (int u = 0; u < U8; u++) {
+                const int j = j0 + NH * u;
+                if (j < tot) {
+                    if (want_uid) c.out.d_unique_ids[(int64_t)off.y + j] = uid[u];
+                    if (want_pos) reinterpret_cast<float4*>(c.out.d_shaded4)[(int64_t)off.y + j] = transform_position(sp, pv[u]);
+                }
+            }
+            if (j0 + NH * U8 - ht >= tot) break;  // warp-uniform: no claim left for any thread
+#pragma unroll
+            for (int u = 0; u < U8; u++) uid[u] = nxt[u];
+            if (want_pos) {
+#pragma unroll
+                for (int u = 0; u < U8; u++)
+                    if (j0 + NH * (U8 + u) < tot) pv[u] = __ldg(sp.pos4 + uid[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U8; u++) nxt[u] = j0 + NH * (2 * U8 + u) < tot ? __ldcg(claims + j0 + NH * (2 * U8 + u)) : 0u;
+            if (want_pos) {
+#pragma unroll
+                for (int u = 0; u < U8; u++)
+                    if (j0 + NH * (2 * U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
+            }
+        }
+        VR_MARK(10);
+        // attribute pass-through and per-vertex tally (strategies.py:485-489): one compact loop
+        if ((sp.attr_words && c.out.d_shaded_attr) || c.out.d_shade_counts) {
+#pragma unroll 1
+            for (int j = ht; j < tot; j += NH) {
+                const uint32_t id = __ldcg(claims + j);
+                if (sp.attr_words && c.out.d_shaded_attr) {
+#pragma unroll 1
+                    for (int w = 0; w < sp.attr_words; w++)
+                        c.out.d_shaded_attr[((int64_t)off.y + j) * sp.attr_words + w] = __ldg(sp.attr + (int64_t)id * sp.attr_words + w);
+                }
+                if (c.out.d_shade_counts) atomicAdd(&c.out.d_shade_counts[id], 1);
+            }
+        }
+        // round tables (strategies.py:114-129, flattened): one thread per row
+        if (ht < T) {
+            const int sb = stile * T + ht;
+            const int nr = (int)(m1 >> 16);
+            if (sb < c.n_batches) {
+                const int r0w = off.x + (int)(m1 & 0xFFFFu);
+                int run = off.y + (int)(m0 & 0xFFFFu);
+                if (c.out.d_batch_round_off) c.out.d_batch_round_off[sb] = r0w;
+#pragma unroll 1
+                for (int q = 0; q < nr; q++) {
+                    const uint32_t wv = __ldcg(sc + 2 * T + q * T + ht);
+                    if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0w + q] = run;
+                    if (c.out.d_round_prims) c.out.d_round_prims[r0w + q] = (int)(wv >> 8);
+                    run += (int)(wv & 0xFFu);
+                }
+            }
+        }
+    }
+}
+
 template <int W, bool PREFETCH>
 __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, int bs, RowsGeom g, ShaderParams sp) {
     constexpr int S = 2 * W;
     constexpr int LOG2W = W == 4 ? 2 : W == 8 ? 3 : W == 16 ? 4 : W == 32 ? 5 : 6;
     constexpr int LOG2S = LOG2W + 1;
-    constexpr int T = kRowThreads, NT = kRowCtaThreads;
-    constexpr int kLookbackWarp = T / 32;  // first helper warp
+    constexpr int T = kRowThreads, NT = kRowCtaThreads, NH = NT - T;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) unsigned long long s_bar;
     __shared__ int s_tile;
     __shared__ int2 s_warp_tot[T / 32];  // (rounds, claims) of each dedup warp
-    __shared__ int2 s_base;              // output offsets of the tile (look-back result)
-    __shared__ int s_cnt[T], s_ex[T + 1];  // claims of each row, exclusive prefix over the tile
+    __shared__ int2 s_base;              // output offsets of the tile being shaded (look-back result)
+    __shared__ int s_cnt[T], s_ex[T];    // claims of each row, exclusive prefix inside the row's dedup warp
+    __shared__ int s_rnd[T], s_rex[T];   // rounds of each row, exclusive prefix inside the row's dedup warp
+    int t = threadIdx.x;
+    asm volatile("" : "+r"(t));
+    const int lane = t & 31, wid = t >> 5;
+    const bool dedup_thread = t < T;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem_raw);
     const uint32_t row_bytes = 4u * (uint32_t)g.row_words;
-    const uint32_t a_tab0 = sbase + row_bytes * T;                         // table, later the flat claim list
+    const uint32_t a_row = sbase + row_bytes * t;                          // claims from word 0
+    const uint32_t a_ids = a_row + 4u * (uint32_t)g.slack;                 // indices of the batch
+    const uint32_t a_tab0 = sbase + row_bytes * T;                         // table
+    const uint32_t a_idtab = a_tab0 + 4u * t;                              // + 4*T*slot
+    const uint32_t a_ranks0 = a_tab0 + 4u * T * S;                         // rank rows
+    const uint32_t a_ranks = a_ranks0 + (uint32_t)g.rk_stride * t;
+    const uint32_t a_rounds0 = a_ranks0 + (uint32_t)g.rk_stride * T;       // round records [round][thread]
+    const uint32_t a_rounds = a_rounds0 + 4u * t;
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
+
 #ifdef VR_TIMELINE
     const unsigned long long t_entry = timeline_now();
 #endif
     // static batching (batching.py:76-84): batch b = [first + b * bs, min(.. + bs, last_end)); the two
     // uniform loads overlap the ticket; the caller's claim is verified off the critical path below
     const int first = __ldg(c.bbegin), last_end = __ldg(c.bend + (c.n_batches - 1));
-    for (uint32_t o = 16u * threadIdx.x; o < (uint32_t)(4 * S * T); o += 16u * NT)  // tag 0 = never used
+    for (uint32_t o = 16u * t; o < (uint32_t)(4 * S * T); o += 16u * NT)  // tag 0 = never used
         asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a_tab0 + o), "r"(0u) : "memory");
-    if (threadIdx.x == 0) {
+    if (t == 0) {
         s_tile = (int)atomicAdd((unsigned long long*)&c.acc[ACC_TICKET], 1ull);  // tiles in ticket order
         mbar_init(bar, T);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int tile = s_tile;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    int t = threadIdx.x;
-    asm volatile("" : "+r"(t));
-    const bool dedup_thread = t < T;
-    const uint32_t a_row = sbase + row_bytes * t;                          // claims from word 0
-    const uint32_t a_ids = a_row + 4u * (uint32_t)g.slack;                 // indices of the batch
-    const uint32_t a_idtab = a_tab0 + 4u * t;                              // + 4*T*slot
-    const uint32_t a_ranks0 = a_tab0 + 4u * T * S;                         // rank rows
-    const uint32_t a_ranks = a_ranks0 + (uint32_t)g.rk_stride * t;
-    const uint32_t a_rounds = a_ranks0 + (uint32_t)g.rk_stride * T + 4u * t;  // + 4*T*round
+    const int tile = s_tile;                 // this CTA dedups tile `tile` ...
+    const int stile = tile - g.lag;          // ... and shades tile `stile`
+    const bool has_tile = tile < g.n_tiles;
+    const bool has_stile = stile >= 0 && stile < g.n_tiles;
 #ifdef VR_TIMELINE
     VR_MARK_AT(0, t_entry);
 #endif
     VR_MARK(1);
-    const int b = tile * T + t;
-    bool active = false;
-    int rt_prefix = 0, rt_rounds = 0;  // this row's rounds: exclusive prefix inside its warp, count
+    uint32_t* __restrict__ my_scratch = c.stage_uid + (size_t)tile * (size_t)g.tile_words;
 
     if (dedup_thread) {
-        active = b < c.n_batches;
+        const int b = tile * T + t;
+        bool active = has_tile && b < c.n_batches;
         const int begin = first + b * bs;
         int n = active ? min(bs, last_end - begin) : 0;
-        // memory safety of the staged copy does not depend on the batch arrays
-        if (active && (first < 0 || (first & 3) || n <= 0 || (int64_t)begin + n > c.n_idx || n % 3 != 0 || bs > c.max_span)) {
+        // memory safety of the staged copy does not depend on the caller's batch arrays
+        if (active && (first < 0 || (first & 3) || n <= 0 || (int64_t)begin + n > c.n_idx || n % 3 != 0 || n > c.max_span)) {
             report_error(c, b, first < 0 || (first & 3) || n <= 0 || (int64_t)begin + n > c.n_idx || n % 3 != 0 ? VR_ERR_BAD_BATCH : VR_ERR_UNSUPPORTED);
             active = false;
             n = 0;
@@ -164,12 +360,12 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         // ---- A: stage the row
         {
             const uint32_t bytes = (n & 3) == 0 ? 4u * (uint32_t)n : 0u;
-            mbar_arrive_expect_tx(bar, bytes);
-            if (bytes) {
-                bulk_g2s(a_ids, c.idx + begin, bytes, bar);
-            } else {
+            if (!bytes) {
+#pragma unroll 1
                 for (int i = 0; i < n; i++) sts_u32(a_ids + 4 * i, __ldg(c.idx + begin + i));  // short last batch
             }
+            mbar_arrive_expect_tx(bar, bytes);
+            if (bytes) bulk_g2s(a_ids, c.idx + begin, bytes, bar);
         }
         mbar_wait(bar, 0);
         VR_MARK(2);
@@ -183,53 +379,57 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         // max-over-lanes(slots + collisions + replays) trips, not the sum of per-slot maxima.
         //   table: entry[slot][thread] = id << 8 | round tag << LOG2W | rank, one 32-bit shared load
         //   per probe; a slot is occupied iff its tag is the current round's, so a new round clears
-        //   nothing (tag 0 = never used; ids must fit 24 bits, checked below).
+        //   nothing (tag 0 = never used; ids must fit 24 bits: the helper warps check every index).
         // The trip is software-pipelined by hand: the probe and the next slot's id for trip i+1 are
-        // loaded as soon as the lane's next state is known, and the side effects of trip i (claim
-        // list, local index, counters, L2 prefetch of the claimed vertex) issue under that latency.
-        // Side-effect stores go to a per-thread dummy word when the lane does not take them, so the
-        // only branches are the loop and the (rare) round end.
+        // loaded as soon as the lane's next state is known, and the side effects of trip i issue
+        // under that latency.  The table store goes to a per-thread dummy word when the lane does
+        // not claim, so the only branches are the loop and the (rare) round end.
         constexpr uint32_t kTagInc = 1u << LOG2W;
         constexpr uint32_t kTagMask = 0xFFu & ~(uint32_t)(W - 1);
         const uint32_t a_dummy = a_rounds + 4u * T * (uint32_t)g.max_rounds;  // one spare word per thread
-        int p = 0, fill = 0, cursor = 0, stop = n, rounds = 0;
+        int p = 0, fill = 0, cursor = 0, rounds = 0;
         uint32_t cl = a_row;  // next claim slot of the row
         uint32_t tagw = kTagInc;
         uint32_t ax = a_ids;  // address of slot p
         uint32_t x = lds_u32(ax);
-        uint32_t bad = n > 0 ? (x >> 24) : 0u;
+        // every index is range-checked as it becomes the lane's current slot: the packed table entry
+        // holds 24 bits (vertex_count <= 2^24 on this path) and the gather must stay inside the buffer
+        const uint32_t vcount = (uint32_t)sp.vertex_count;
+        bool bad = n > 0 && x >= vcount;
         uint32_t h = (x * 0x9E3779B1u) >> (32 - LOG2S);
-        uint32_t v = lds_u32(a_idtab + 4u * T * h), cand = lds_u32(ax + 4);
+        uint32_t ai = a_idtab + 4u * T * h;  // address of the probed table slot
+        uint32_t v = lds_u32(ai), cand = lds_u32(ax + 4);
         for (;;) {
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const bool live = p < n;
-                const uint32_t ai = a_idtab + 4u * T * h;
                 const uint32_t xk = (x << 8) | tagw;
                 const uint32_t tq = v ^ xk;                       // == rank (< W) iff the slot holds x in this round
                 const bool hit = tq < (uint32_t)W;
                 const bool fre = (tq & kTagMask) != 0;            // slot not used in this round
-                // round end before slot p: the fetch that filled the warp is exhausted (p >= stop), or x is
-                // the first id that cannot be assigned (free slot reached with all W lanes claimed)
-                const bool ends = live & ((p >= stop) | (fre & (fill == W)));
+                // The round ends before slot p once all W lanes are claimed and either x is the first id
+                // that cannot be assigned (free slot reached), or the W-wide fetch in which the last
+                // claim was made is exhausted: fetches start at cursor, cursor + W, ... and a new one
+                // starts only while a lane is free (strategies.py:201, :220).
+                const bool ends = live & (fill == W) & (fre | (((p - cursor) & (W - 1)) == 0));
                 const bool adv = live & (hit | fre) & !ends;
                 const bool clm = adv & fre;  // strategies.py:207-212: new id -> lowest free lane
                 sts_u32(clm ? ai : a_dummy, xk | (uint32_t)fill);  // before the next probe is loaded
                 const uint32_t xn = adv ? cand : x;
                 const uint32_t hx = (xn * 0x9E3779B1u) >> (32 - LOG2S);
                 const uint32_t hn = (hit | fre) ? hx : ((h + 1) & (S - 1));
-                const int pn = p + (adv ? 1 : 0);
+                const uint32_t ain = a_idtab + 4u * T * hn;
                 const uint32_t axn = ax + (adv ? 4u : 0u);
-                uint32_t vn = lds_u32(a_idtab + 4u * T * hn), candn = lds_u32(axn + 4);
-                const uint32_t r = hit ? tq : (uint32_t)fill;
-                sts_u32(clm ? cl : a_dummy, x);
-                sts_u8(adv ? a_ranks + (uint32_t)p : a_dummy, r);
-                if (PREFETCH && clm) prefetch_l2(sp.pos4 + x);
+                uint32_t vn = lds_u32(ain), candn = lds_u32(axn + 4);
+                // claim list and local index: written unconditionally, a lane that does not resolve slot
+                // p here overwrites both when it does (the addresses only move on adv / clm)
+                sts_u32(cl, x);
+                sts_u8(a_ranks + (uint32_t)p, hit ? tq : (uint32_t)fill);
                 cl += clm ? 4u : 0u;
                 fill += clm ? 1 : 0;
-                if (clm && fill == W) stop = min(n, cursor + (((p - cursor) >> LOG2W) + 1) * W);  // end of this fetch
-                if (pn < n) bad |= xn >> 24;
-                p = pn; ax = axn; x = xn; h = hn;
+                p += adv ? 1 : 0;
+                bad |= (p < n) & (xn >= vcount);
+                ax = axn; x = xn; h = hn; ai = ain;
                 if (ends) {
                     const int d = p - cursor;
                     const int emitted = (int)(((uint32_t)d * 43691u) >> 17);  // d / 3 for d < 2^16
@@ -237,17 +437,18 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                     rounds++;
                     fill = 0;
                     cursor += 3 * emitted;
-                    stop = n;
                     p = cursor;  // re-open at the first unconsumed slot (the row still holds it: see slack)
                     ax = a_ids + 4u * (uint32_t)p;
                     x = lds_u32(ax);
                     h = (x * 0x9E3779B1u) >> (32 - LOG2S);
+                    ai = a_idtab + 4u * T * h;
                     if (tagw == kTagMask) {  // tag space exhausted: wipe this thread's column
+#pragma unroll 1
                         for (int k = 0; k < S; k++) sts_u32(a_idtab + 4u * T * k, 0u);
                         tagw = 0;
                     }
                     tagw += kTagInc;
-                    vn = lds_u32(a_idtab + 4u * T * h);
+                    vn = lds_u32(ai);
                     candn = lds_u32(ax + 4);
                 }
                 v = vn; cand = candn;
@@ -255,8 +456,8 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
             if (!__any_sync(0xffffffffu, p < n)) break;
         }
         VR_MARK(3);
-        if (active && bad) {  // an id does not fit the packed table entry
-            report_error(c, b, VR_ERR_UNSUPPORTED);
+        if (active && bad) {
+            report_error(c, b, VR_ERR_BAD_BATCH);  // index outside the vertex buffer
             active = false;
         }
         if (active && (claimed_begin != begin || claimed_end != begin + n)) {
@@ -271,72 +472,48 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         const int inc_r = warp_incl_scan(my_r, lane), inc_u = warp_incl_scan(my_u, lane);
         if (lane == 31) s_warp_tot[wid] = make_int2(inc_r, inc_u);
         s_cnt[t] = my_u;
-        s_ex[t] = inc_u - my_u;  // exclusive inside the warp; made tile-wide after the barrier
-        rt_prefix = inc_r - my_r;
-        rt_rounds = my_r;
-        __syncthreads();  // the tile's dedup is done
-        if (wid == 1) s_ex[t] += s_warp_tot[0].y;
-        if (t == T - 1) s_ex[T] = s_warp_tot[0].y + s_warp_tot[1].y;
+        s_ex[t] = inc_u - my_u;  // + s_warp_tot[0].y for rows of warp 1
+        s_rnd[t] = my_r;
+        s_rex[t] = inc_r - my_r;
     } else {
-        __syncthreads();  // the tile's dedup is done
-    }
-
-    if (wid == kLookbackWarp) {
-        // ---- C (first helper warp): output offsets by decoupled look-back over tiles
-        const int ar = s_warp_tot[0].x + s_warp_tot[1].x, au = s_warp_tot[0].y + s_warp_tot[1].y;
-        volatile unsigned long long* state = c.tile_state;
-        if (lane == 0) {
-            __threadfence();  // errors reported by this tile are visible before its state
-            state[tile] = kStateAggregate | ((unsigned long long)(uint32_t)ar << 32) | (uint32_t)au;
-        }
-        long long er = 0, eu = 0;  // exclusive prefix of this tile
-        bool lost = false;
-        for (int pz = tile - 1; pz >= 0; pz -= 32) {
-            const int idx = pz - lane;
-            unsigned long long word = kStateInclusive;  // tiles before the first one: inclusive zero
-            int spins = 0;
-            for (;;) {
-                if (idx >= 0) word = state[idx];
-                if (!__any_sync(0xffffffffu, (word >> 62) == 0)) break;
-                if (++spins > (1 << 20)) { lost = true; break; }
-                __nanosleep(20);
-            }
-            if (lost) break;
-            const uint32_t incl = __ballot_sync(0xffffffffu, (word >> 62) == 2);
-            const int upto = incl ? __ffs(incl) - 1 : 31;  // nearest predecessor holding an inclusive prefix
-            long long vr = lane <= upto ? (long long)((word >> 32) & 0x3FFFFFFFull) : 0;
-            long long vu = lane <= upto ? (long long)(word & 0xFFFFFFFFull) : 0;
+        // ================= helper warps: tile `stile` =================
+        const int ht = t - T;  // 0..127
+        const uint32_t vcount_h = (uint32_t)sp.vertex_count;
+        if (has_stile) prefetch_l2(c.stage_uid + (size_t)stile * (size_t)g.tile_words + 32 * ht);  // its scratch: 16 KB
+        // ---- F (optional): the vertices of tile `tile` are prefetched into L2; they are gathered ~K
+        // tiles later.  One request per distinct 32-byte sector among the 32 indices of a step.
+        if (PREFETCH && has_tile) {
+            const int64_t tb = (int64_t)first + (int64_t)tile * T * bs;
+            const int tn = (int)max((int64_t)0, min((int64_t)T * bs, (int64_t)last_end - tb));
+            constexpr int HU = 4;
+            for (int j0 = ht; j0 - lane < tn; j0 += HU * NH) {  // warp-uniform trip count
+                uint32_t id[HU];
 #pragma unroll
-            for (int d = 16; d > 0; d >>= 1) {
-                vr += __shfl_xor_sync(0xffffffffu, vr, d);
-                vu += __shfl_xor_sync(0xffffffffu, vu, d);
+                for (int u = 0; u < HU; u++) id[u] = j0 + u * NH < tn ? __ldg(c.idx + tb + j0 + u * NH) : 0xFFFFFFFFu;
+#pragma unroll
+                for (int u = 0; u < HU; u++) {
+                    const bool ok = id[u] < vcount_h;
+                    const uint32_t same = __match_any_sync(0xffffffffu, ok ? (id[u] >> 1) : 0xFFFFFFFFu);
+                    if (ok && (uint32_t)lane == (uint32_t)(__ffs(same) - 1)) prefetch_l2(sp.pos4 + id[u]);
+                }
             }
-            er += vr;
-            eu += vu;
-            if (incl) break;
         }
-        if (lane == 0) {
-            if (lost) report_error(c, (int64_t)tile * T, VR_ERR_CUDA);
-            const long long R = er + ar, U = eu + au;
-            state[tile] = kStateInclusive | ((unsigned long long)(R & 0x3FFFFFFF) << 32) | (unsigned long long)(U & 0xFFFFFFFFll);
-            const bool fits = U <= c.out.cap_unique && R <= c.out.cap_rounds && U <= 0x7fffffffLL && !lost;
-            if (!fits) report_error(c, (int64_t)tile * T, VR_ERR_CAPACITY);
-            s_base = fits ? make_int2((int)er, (int)eu) : make_int2(-1, -1);
-            if (tile == c.n_fused_tiles - 1) { __threadfence(); finish_stats(c, R, U); }
-        }
-    } else {
-        asm volatile("bar.sync 1, %0;" ::"n"(kRowCtaThreads - 32) : "memory");  // s_ex is tile-wide now (5 warps)
+        VR_MARK(7);
+        if (has_stile) rows_shade_tile<0>(c, g, sp, stile, ht, &s_base);
+        VR_MARK(6);
     }
-    if (wid != kLookbackWarp && c.out.d_assembly_map) {
-        // ---- C (other warps): local indices.  chunk = 8 slots of one row -> one 16-byte store;
-        // consecutive threads write consecutive chunks of the tile's contiguous piece of the map
-        const int pt = t < T ? t : t - 32;
-        constexpr int NP = NT - 32;
+    __syncthreads();  // tile's dedup done (and the helpers are back)
+    VR_MARK(4);
+    if (!has_tile) return;
+
+    // ---- C: post.  Local indices: chunk = 8 slots of one row -> one 16-byte store; consecutive
+    // threads write consecutive chunks of the tile's contiguous piece of the assembly map.
+    if (c.out.d_assembly_map) {
         const int cpr = bs >> 3;
         uint16_t* __restrict__ amap = c.out.d_assembly_map + (int64_t)tile * T * bs;
         const int64_t slots_left = (int64_t)last_end - first - (int64_t)tile * T * bs;
         const int chunks = (int)min((int64_t)T * cpr, (slots_left + 7) >> 3);
-        for (int ch = pt; ch < chunks; ch += NP) {
+        for (int ch = t; ch < chunks; ch += NT) {
             const int row = (int)__umulhi((uint32_t)ch, g.cpr_magic);
             const int qo = ch - row * cpr;
             const uint32_t ra = a_ranks0 + (uint32_t)g.rk_stride * row + 8u * qo;
@@ -350,98 +527,71 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                 *reinterpret_cast<uint4*>(amap + 8 * (int64_t)ch) = o;
             } else {
                 const uint32_t w4[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll 1
                 for (int k = 0; k < 8 && (int64_t)8 * ch + k < slots_left; k++)
                     amap[8 * (int64_t)ch + k] = (uint16_t)(w4[k >> 1] >> (16 * (k & 1)));
             }
         }
     }
-
-    // ---- C/D: compaction of the rows' claims into a flat list, then shading by all warps.  The flat
-    // list lives in the table's shared memory (S * T words); tiles whose claims do not fit (every
-    // index unique, e.g. a shuffled mesh) are taken in several groups of rows.
-    const bool want_uid = c.out.d_unique_ids != nullptr;
-    const bool want_pos = sp.kind == VR_SHADER_POSITION;
-    const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
-    const bool want_cnt = c.out.d_shade_counts != nullptr;
-    constexpr int kCap = S * T;
-    int2 off = make_int2(0, 0);
-    for (int r0 = 0, pass = 0; r0 < T; pass++) {
-        if (pass > 0) __syncthreads();  // the flat list of the previous group was consumed
-        const int base = s_ex[r0];
-        int r1 = r0 + 1;
-        if (s_ex[T] - base <= kCap) r1 = T;
-        else while (r1 < T && s_ex[r1 + 1] - base <= kCap) r1++;
-        // the look-back warp of pass 0 is still busy: the other five warps copy, one row per warp
-        if (pass > 0 || wid != kLookbackWarp) {
-            const int cw = pass > 0 ? wid : (wid < kLookbackWarp ? wid : wid - 1);
-            const int ncw = pass > 0 ? NT / 32 : NT / 32 - 1;
-            for (int r = r0 + cw; r < r1; r += ncw) {
-                const int cnt = s_cnt[r];
-                const uint32_t src = sbase + row_bytes * (uint32_t)r, dst = a_tab0 + 4u * (uint32_t)(s_ex[r] - base);
-                for (int k = lane; k < cnt; k += 32) sts_u32(dst + 4u * k, lds_u32(src + 4u * k));
-            }
-        }
-        __syncthreads();
-        if (pass == 0) {
-            VR_MARK(4);
-            off = s_base;
-            if (off.x < 0) return;  // offsets unknown or outputs too small: leave the outputs untouched
-            if (dedup_thread && active) {  // round tables (strategies.py:114-129, flattened)
-                const int r0w = off.x + rt_prefix + (wid == 1 ? s_warp_tot[0].x : 0);
-                int run = off.y + s_ex[t];
-                if (c.out.d_batch_round_off) c.out.d_batch_round_off[b] = r0w;
-                for (int q = 0; q < rt_rounds; q++) {
-                    const uint32_t wv = lds_u32(a_rounds + 4u * T * q);
-                    if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0w + q] = run;
-                    if (c.out.d_round_prims) c.out.d_round_prims[r0w + q] = (int)(wv >> 8);
-                    run += (int)(wv & 0xFFu);
-                }
-            }
-        }
-        const int tot = s_ex[r1] - base;
-        const int64_t o0 = (int64_t)off.y + base;
-        uint32_t* __restrict__ out_uid = c.out.d_unique_ids + o0;
-        float4* __restrict__ shaded = reinterpret_cast<float4*>(c.out.d_shaded4) + o0;
-        constexpr int U4 = 4;
-        for (int j0 = t; j0 < tot; j0 += NT * U4) {
-            uint32_t uid[U4];
-            float4 pv[U4];
-#pragma unroll
-            for (int u = 0; u < U4; u++) {
-                const int j = j0 + NT * u;
-                uid[u] = j < tot ? lds_u32(a_tab0 + 4u * (uint32_t)j) : 0u;
-            }
-            if (want_pos) {
-#pragma unroll
-                for (int u = 0; u < U4; u++)
-                    if (j0 + NT * u < tot) pv[u] = __ldg(sp.pos4 + uid[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < U4; u++) {
-                const int j = j0 + NT * u;
-                if (j >= tot) continue;
-                if (want_uid) out_uid[j] = uid[u];
-                if (want_pos) shaded[j] = transform_position(sp, pv[u]);
-                if (want_attr)
-                    for (int q = 0; q < sp.attr_words; q++)
-                        c.out.d_shaded_attr[(o0 + j) * sp.attr_words + q] = __ldg(sp.attr + (int64_t)uid[u] * sp.attr_words + q);
-                if (want_cnt) atomicAdd(&c.out.d_shade_counts[uid[u]], 1);
-            }
-        }
-        r0 = r1;
+    // Scratch: meta0[r] = claim prefix | claims << 16, meta1[r] = round prefix | rounds << 16 (both
+    // tile-wide), round records [q][r], then the rows' claims back to back.
+    const int w0r = s_warp_tot[0].x, w0u = s_warp_tot[0].y;
+    if (t < T) {
+        const int exu = s_ex[t] + (t >= 32 ? w0u : 0), exr = s_rex[t] + (t >= 32 ? w0r : 0);
+        my_scratch[t] = (uint32_t)exu | ((uint32_t)s_cnt[t] << 16);
+        my_scratch[T + t] = (uint32_t)exr | ((uint32_t)s_rnd[t] << 16);
     }
+    for (int k = t; k < T * g.max_rounds; k += NT)  // [round][row] in shared memory and in the scratch
+        my_scratch[2 * T + k] = lds_u32(a_rounds0 + 4u * (uint32_t)k);
+    {
+        uint32_t* __restrict__ claims = my_scratch + T * (2 + g.max_rounds);
+#pragma unroll 1
+        for (int r0 = 2 * wid; r0 < T; r0 += 2 * (NT / 32)) {  // two rows per warp and step
+            const int c0 = s_cnt[r0], c1 = s_cnt[r0 + 1];
+            const int e0 = s_ex[r0] + (r0 >= 32 ? w0u : 0), e1 = s_ex[r0 + 1] + (r0 >= 32 ? w0u : 0);
+            const uint32_t src0 = sbase + row_bytes * (uint32_t)r0, src1 = src0 + row_bytes;
+            for (int k = lane; k < max(c0, c1); k += 32) {
+                const uint32_t v0 = k < c0 ? lds_u32(src0 + 4u * k) : 0u, v1 = k < c1 ? lds_u32(src1 + 4u * k) : 0u;
+                if (k < c0) claims[e0 + k] = v0;
+                if (k < c1) claims[e1 + k] = v1;
+            }
+        }
+    }
+    __threadfence();  // release: scratch (and reported errors) before the aggregate
+    __syncthreads();
+    if (t == 0)
+        st_relaxed_gpu_u64(c.tile_state + tile, kStateAggregate | ((unsigned long long)(uint32_t)(w0r + s_warp_tot[1].x) << 32) | (uint32_t)(w0u + s_warp_tot[1].y));
     VR_MARK(5);
 }
 
+// The last K tiles have no later CTA to shade them: a light kernel (no shared-memory rows, all of
+// them resident at once) does it after the tile kernel.
+__global__ void __launch_bounds__(kRowCtaThreads - kRowThreads) rows_drain_kernel(RunCtx c, RowsGeom g, ShaderParams sp, int first_tile) {
+    __shared__ int2 s_base;
+    rows_shade_tile<0>(c, g, sp, first_tile + (int)blockIdx.x, (int)threadIdx.x, &s_base);
+}
+
 template <int W>
-static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g, const ShaderParams& sp, cudaStream_t stream) {
-    const int blocks = (int)ceil_div(c.n_batches, kRowThreads);
-    if (sp.kind == VR_SHADER_POSITION) {  // claims prefetch their vertex into L2 for the shading phase
-        VR_CUDA_CHECK(cudaFuncSetAttribute(warp_rows_kernel<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
-        warp_rows_kernel<W, true><<<blocks, kRowCtaThreads, g.smem, stream>>>(c, bs, g, sp);
-    } else {
-        VR_CUDA_CHECK(cudaFuncSetAttribute(warp_rows_kernel<W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
-        warp_rows_kernel<W, false><<<blocks, kRowCtaThreads, g.smem, stream>>>(c, bs, g, sp);
-    }
+static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const ShaderParams& sp, cudaStream_t stream) {
+    // Optional: prefetch the vertices of a tile into L2 when it is deduplicated (VR_PREFETCH=1).  Off by
+    // default: on the B200 the gathers ~K tiles later are L2 hits or overlap the next tile's dedup
+    // anyway, and the extra L2 requests cost more than they save (profiles/README.md).
+    const char* pf = getenv("VR_PREFETCH");
+    const bool prefetch = sp.kind == VR_SHADER_POSITION && pf && pf[0] == '1';
+    auto kernel = prefetch ? warp_rows_kernel<W, true> : warp_rows_kernel<W, false>;
+    RowsGeom g = g_in;
+    VR_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRowCtaThreads, g.smem);
+    g.n_tiles = (int)ceil_div(c.n_batches, kRowThreads);
+    const char* e = getenv("VR_LAG");
+    const int resident = sms * (per_sm > 0 ? per_sm : 1);
+    g.lag = e ? atoi(e) : 2 * resident;  // the tile a CTA shades was finished a whole wave of CTAs ago: no waiting
+    if (g.lag > g.n_tiles) g.lag = g.n_tiles;
+    if (g.lag < 1) g.lag = 1;
+    kernel<<<g.n_tiles, kRowCtaThreads, g.smem, stream>>>(c, bs, g, sp);
+    rows_drain_kernel<<<g.lag, kRowCtaThreads - kRowThreads, 0, stream>>>(c, g, sp, g.n_tiles - g.lag);
     return VR_OK;
 }

@@ -1,6 +1,6 @@
 #!/usr/bin/env python
-"""Debugging aid: build libvrgeom with -DVR_TIMELINE into a scratch .so, run the headline workload once
-and print per-phase durations of the tile kernel (median / p10 / p90 over tiles, microseconds)."""
+"""Debugging aid: build libvrgeom with -DVR_TIMELINE into a scratch .so, run the headline workload and
+print per-phase durations of the tile kernel (median / p10 / p90 over tiles, microseconds)."""
 import ctypes as C, os, subprocess, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -27,25 +27,33 @@ spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=pos4, matrix=M, v
 bufs = engine.RunBuffers()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
-    flush.zero_()
+    if not os.environ.get("VR_NOFLUSH"): flush.zero_()
     run = engine.run_device("warp", d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 96, cfg, None, spec, buffers=bufs, static=True)
 torch.cuda.synchronize()
 run.check()
 lib = N.lib()
-MARKS, TILES = 6, 4096
+MARKS, TILES = 12, 8192
 buf = (C.c_ulonglong * (MARKS * 2 * TILES))()
 lib.vr_debug_timeline.restype = C.c_int
 got = lib.vr_debug_timeline(buf, MARKS * 2 * TILES)
 a = np.frombuffer(buf, dtype=np.uint64).reshape(MARKS, 2, TILES).astype(np.int64)
-nt = min(TILES, (nb + 63) // 64)
-a = a[:, :, :nt]
-t0 = a[0].min()
-names = ["entry->ticket", "ticket->staged", "dedup", "lookback+amap", "shade"]
-print(f"tiles {nt}, kernel span {(a[5].max() - t0) / 1e3:.1f} us")
-for k in range(5):
-    d = (a[k + 1] - a[k]).reshape(-1) / 1e3
-    print(f"{names[k]:16s} median {np.median(d):7.2f}  p10 {np.percentile(d, 10):7.2f}  p90 {np.percentile(d, 90):7.2f}  mean {d.mean():7.2f} us")
-life = (a[5] - a[0]).reshape(-1) / 1e3
-print(f"{'lifetime':16s} median {np.median(life):7.2f}  p10 {np.percentile(life, 10):7.2f}  p90 {np.percentile(life, 90):7.2f}  mean {life.mean():7.2f} us")
-start = (a[0][0] - t0) / 1e3
-print("tile start times (us) at tile 0, 592, 1184, ...:", [round(float(start[i]), 1) for i in range(0, nt, 592)])
+nt = (nb + 63) // 64
+t0 = a[0, 0, :nt].min()
+def stat(name, d):
+    d = d.reshape(-1) / 1e3
+    print(f"  {name:28s} median {np.median(d):7.2f}  p10 {np.percentile(d, 10):7.2f}  p90 {np.percentile(d, 90):7.2f}  mean {d.mean():7.2f} us")
+d = a[:, 0, :nt]
+print(f"tiles {nt}; dedup warp 0 (CTAs that own a tile); span to last publish {(d[5].max() - t0) / 1e3:.1f} us")
+for k, nm in enumerate(["entry->ticket", "ticket->staged", "dedup", "wait for helpers", "post (indices, scratch, publish)"]):
+    stat(nm, d[k + 1] - d[k])
+stat("lifetime", d[5] - d[0])
+h = a[:, 1, :]
+sel = np.arange(592, nt)  # CTAs whose helpers shade a tile and check a tile
+print("helper warp 2")
+stat("range check", h[7, sel] - h[1, sel])
+stat("look-back + shading", h[6, sel] - h[7, sel])
+stat("  wait aggregate + fence", h[8, sel] - h[7, sel])
+stat("  ids, gathers, look-back", h[9, sel] - h[8, sel])
+stat("  stores + further steps", h[10, sel] - h[9, sel])
+stat("  round tables", h[6, sel] - h[10, sel])
+print("tile start times (us) at tile 0, 592, 1184, ...:", [round(float((d[0, i] - t0) / 1e3), 1) for i in range(0, nt, 592)])
