@@ -98,6 +98,11 @@ __device__ __forceinline__ unsigned long long ld_relaxed_gpu_u64(const unsigned 
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void st_relaxed_gpu_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -141,12 +146,10 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
     {
         int spins = 0;
         for (;;) {
-            if (lane == 0) mine = ld_relaxed_gpu_u64(c.tile_state + stile);
-            mine = __shfl_sync(0xffffffffu, mine, 0);
-            if (mine >> 62) break;
+            mine = ld_acquire_gpu_u64(c.tile_state + stile);  // every thread acquires: the scratch is visible to it
+            if (__all_sync(0xffffffffu, (mine >> 62) != 0)) break;
             if (++spins > (1 << 22)) { lost = true; break; }
         }
-        __threadfence();  // acquire
     }
     VR_MARK(8);
     const int tot = lost ? 0 : (int)(mine & 0xFFFFFFFFull) ;
@@ -559,6 +562,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
     }
     __threadfence();  // release: scratch (and reported errors) before the aggregate
     __syncthreads();
+    if (t == 0) __threadfence();
     if (t == 0)
         st_relaxed_gpu_u64(c.tile_state + tile, kStateAggregate | ((unsigned long long)(uint32_t)(w0r + s_warp_tot[1].x) << 32) | (uint32_t)(w0u + s_warp_tot[1].y));
     VR_MARK(5);
