@@ -548,23 +548,21 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         my_scratch[2 * T + k] = lds_u32(a_rounds0 + 4u * (uint32_t)k);
     {
         uint32_t* __restrict__ claims = my_scratch + T * (2 + g.max_rounds);
-#pragma unroll 1
-        for (int r0 = 2 * wid; r0 < T; r0 += 2 * (NT / 32)) {  // two rows per warp and step
-            const int c0 = s_cnt[r0], c1 = s_cnt[r0 + 1];
-            const int e0 = s_ex[r0] + (r0 >= 32 ? w0u : 0), e1 = s_ex[r0 + 1] + (r0 >= 32 ? w0u : 0);
-            const uint32_t src0 = sbase + row_bytes * (uint32_t)r0, src1 = src0 + row_bytes;
-            for (int k = lane; k < max(c0, c1); k += 32) {
-                const uint32_t v0 = k < c0 ? lds_u32(src0 + 4u * k) : 0u, v1 = k < c1 ? lds_u32(src1 + 4u * k) : 0u;
-                if (k < c0) claims[e0 + k] = v0;
-                if (k < c1) claims[e1 + k] = v1;
-            }
+#pragma unroll 2
+        for (int r = wid; r < T; r += NT / 32) {  // one row per warp and step
+            const int cnt = s_cnt[r];
+            const int e = s_ex[r] + (r >= 32 ? w0u : 0);
+            const uint32_t* __restrict__ rowp = reinterpret_cast<const uint32_t*>(smem_raw + (size_t)row_bytes * r);
+            for (int k = lane; k < cnt; k += 32) claims[e + k] = rowp[k];
         }
     }
-    __threadfence();  // release: scratch (and reported errors) before the aggregate
+    // release: the barrier orders every thread's scratch writes (and reported errors) before thread
+    // 0's cumulative gpu-scope fence, which orders them before the aggregate
     __syncthreads();
-    if (t == 0) __threadfence();
-    if (t == 0)
+    if (t == 0) {
+        __threadfence();
         st_relaxed_gpu_u64(c.tile_state + tile, kStateAggregate | ((unsigned long long)(uint32_t)(w0r + s_warp_tot[1].x) << 32) | (uint32_t)(w0u + s_warp_tot[1].y));
+    }
     VR_MARK(5);
 }
 
@@ -592,7 +590,8 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
     g.n_tiles = (int)ceil_div(c.n_batches, kRowThreads);
     const char* e = getenv("VR_LAG");
     const int resident = sms * (per_sm > 0 ? per_sm : 1);
-    g.lag = e ? atoi(e) : 2 * resident;  // the tile a CTA shades was finished a whole wave of CTAs ago: no waiting
+    g.lag = e ? atoi(e) : resident;  // the tile a CTA shades was finished by a CTA that has (almost surely) left the GPU;
+                                     // a shorter lag makes the helpers wait, a longer one grows the drain kernel
     if (g.lag > g.n_tiles) g.lag = g.n_tiles;
     if (g.lag < 1) g.lag = 1;
     kernel<<<g.n_tiles, kRowCtaThreads, g.smem, stream>>>(c, bs, g, sp);
