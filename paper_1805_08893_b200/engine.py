@@ -156,6 +156,7 @@ class DeviceRun:
         self.unique_ids = self.assembly_map = self.shaded4 = self.shaded_attr = None
         self.shade_counts = None
         self.stats_dev = None
+        self.launches = 0
         self._stats = None
 
     # -- statistics -----------------------------------------------------------------
@@ -316,5 +317,6 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                         span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws),
                         ws.numel(), _stream_ptr())
     raise_status(st)
+    run.launches = lib.vr_last_launch_count()  # kernels this call launched (bench.py's gpu_launches)
     run._keep = (ws, shader)
     return run
