@@ -337,6 +337,10 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    // Programmatic dependent launch: once every CTA of this grid has got this far, the drain kernel
+    // may start filling the SMs that the last wave of tiles leaves idle (its CTAs wait on the tiles'
+    // published aggregates, not on this grid's completion).
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int tile = s_tile;                 // this CTA dedups tile `tile` ...
     const int stile = tile - g.lag;          // ... and shades tile `stile`
     const bool has_tile = tile < g.n_tiles;
@@ -595,6 +599,18 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
     if (g.lag > g.n_tiles) g.lag = g.n_tiles;
     if (g.lag < 1) g.lag = 1;
     kernel<<<g.n_tiles, kRowCtaThreads, g.smem, stream>>>(c, bs, g, sp);
-    rows_drain_kernel<<<g.lag, kRowCtaThreads - kRowThreads, 0, stream>>>(c, g, sp, g.n_tiles - g.lag);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)g.lag);
+        cfg.blockDim = dim3(kRowCtaThreads - kRowThreads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = getenv("VR_NO_PDL") ? 0 : 1;
+        VR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, rows_drain_kernel, c, g, sp, g.n_tiles - g.lag));
+    }
     return VR_OK;
 }
