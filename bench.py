@@ -312,14 +312,22 @@ def main():
         # per-kernel algorithmic bytes: dedup = index read + map write + metadata;
         # shade/finalize = staged id read is not algorithmic: position read + shaded write
         kernel_alg = {"dedup": 4 * n_idx + 2 * n_idx + 12 * nb, "shade_finalize": 32 * inv}
-        dom_name = "fused dedup+offsets+shade" if fused else N.PROFILE_STAGE_NAMES[dom]
+        dom_name = ("tile kernel (stage + dedup + decoupled look-back/shade) + its drain kernel" if launches == 3
+                    else "fused dedup+offsets+shade" if fused else N.PROFILE_STAGE_NAMES[dom])
+        traffic = None  # DRAM bytes per step of the dominant kernel(s), from the committed ncu --set full capture
+        try:
+            tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+            if tj.get("workload") == name and launches == 3:
+                traffic = tj["traffic_bytes_per_step"]
+        except Exception:
+            pass
         dom_alg = alg if fused else kernel_alg.get(dom_name, alg)
         res = {
             "value": value, "ms_per_step": ms_per_step, "wall_s": wall,
             "stage_ms": {N.PROFILE_STAGE_NAMES[i]: round(float(stage_ms[i]), 5) for i in range(N.VR_PROFILE_STAGES)},
             "roofline": {"bound": "hbm", "kernel": dom_name,
                          "achieved": dom_alg / (stage_ms[dom] * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": dom_alg / (stage_ms[dom] * 1e-3) / 1e9 / peak, "traffic": None,
+                         "frac": dom_alg / (stage_ms[dom] * 1e-3) / 1e9 / peak, "traffic": traffic,
                          "peak_source": peak_src, "algorithmic_bytes": dom_alg,
                          "share_of_step": float(stage_ms[dom] / max(stage_ms.sum(), 1e-9))},
             "stage_roofline": {"algorithmic_bytes": alg, "bytes_per_triangle": alg / tris,
