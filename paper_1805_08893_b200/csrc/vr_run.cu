@@ -88,6 +88,7 @@ __device__ __forceinline__ bool validate_batch(const RunCtx& c, int b, int& begi
 // K0
 // ---------------------------------------------------------------------------------
 __global__ void init_kernel(RunCtx c) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the tile kernel may be scheduled; it waits below
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < ACC_WORDS) c.acc[i] = 0;
     if (i < c.n_fused_tiles) c.tile_state[i] = 0ull;

@@ -331,6 +331,8 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
     const int first = __ldg(c.bbegin), last_end = __ldg(c.bend + (c.n_batches - 1));
     for (uint32_t o = 16u * t; o < (uint32_t)(4 * S * T); o += 16u * NT)  // tag 0 = never used
         asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(a_tab0 + o), "r"(0u) : "memory");
+    // launched as a programmatic dependent of init_kernel: everything above overlapped its tail
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (t == 0) {
         s_tile = (int)atomicAdd((unsigned long long*)&c.acc[ACC_TICKET], 1ull);  // tiles in ticket order
         mbar_init(bar, T);
@@ -598,7 +600,19 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
                                      // a shorter lag makes the helpers wait, a longer one grows the drain kernel
     if (g.lag > g.n_tiles) g.lag = g.n_tiles;
     if (g.lag < 1) g.lag = 1;
-    kernel<<<g.n_tiles, kRowCtaThreads, g.smem, stream>>>(c, bs, g, sp);
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)g.n_tiles);
+        cfg.blockDim = dim3(kRowCtaThreads);
+        cfg.dynamicSmemBytes = g.smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = getenv("VR_NO_PDL") ? 0 : 1;
+        VR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, c, bs, g, sp));
+    }
     {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((unsigned)g.lag);
