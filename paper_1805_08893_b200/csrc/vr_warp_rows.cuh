@@ -554,12 +554,28 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         my_scratch[2 * T + k] = lds_u32(a_rounds0 + 4u * (uint32_t)k);
     {
         uint32_t* __restrict__ claims = my_scratch + T * (2 + g.max_rounds);
-#pragma unroll 2
-        for (int r = wid; r < T; r += NT / 32) {  // one row per warp and step
-            const int cnt = s_cnt[r];
-            const int e = s_ex[r] + (r >= 32 ? w0u : 0);
-            const uint32_t* __restrict__ rowp = reinterpret_cast<const uint32_t*>(smem_raw + (size_t)row_bytes * r);
-            for (int k = lane; k < cnt; k += 32) claims[e + k] = rowp[k];
+        constexpr int CG = 4;  // rows per warp and step: independent load -> store chains
+#pragma unroll 1
+        for (int r0 = wid; r0 < T; r0 += CG * (NT / 32)) {
+            int cnt[CG], e[CG];
+#pragma unroll
+            for (int i = 0; i < CG; i++) {
+                const int r = r0 + i * (NT / 32);
+                cnt[i] = r < T ? s_cnt[r] : 0;
+                e[i] = r < T ? s_ex[r] + (r >= 32 ? w0u : 0) : 0;
+            }
+            int most = 0;
+#pragma unroll
+            for (int i = 0; i < CG; i++) most = max(most, cnt[i]);
+            for (int k = lane; k < most; k += 32) {
+                uint32_t v[CG];
+#pragma unroll
+                for (int i = 0; i < CG; i++)  // reading past a row's claims stays inside shared memory
+                    v[i] = lds_u32(sbase + row_bytes * (uint32_t)min(r0 + i * (NT / 32), T - 1) + 4u * (uint32_t)k);
+#pragma unroll
+                for (int i = 0; i < CG; i++)
+                    if (k < cnt[i]) claims[e[i] + k] = v[i];
+            }
         }
     }
     // release: the barrier orders every thread's scratch writes (and reported errors) before thread
