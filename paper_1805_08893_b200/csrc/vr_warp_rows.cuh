@@ -152,8 +152,11 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
         }
     }
     VR_MARK(8);
-    const int tot = lost ? 0 : (int)(mine & 0xFFFFFFFFull) ;
+    // (the claim count is taken from the scratch, not from the state word: the first helper warp
+    // may already have replaced the aggregate by the tile's inclusive prefix when a later warp polls)
     const uint32_t* __restrict__ sc = c.stage_uid + (size_t)stile * (size_t)g.tile_words;
+    const uint32_t mlast = lost ? 0u : __ldcg(sc + T - 1);
+    const int tot = (int)(mlast & 0xFFFFu) + (int)(mlast >> 16);  // prefix + claims of the last row
     const uint32_t* __restrict__ claims = sc + T * (2 + g.max_rounds);
     const bool want_uid = c.out.d_unique_ids != nullptr;
     const bool want_pos = sp.kind == VR_SHADER_POSITION;
@@ -353,6 +356,25 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
     VR_MARK(1);
     uint32_t* __restrict__ my_scratch = c.stage_uid + (size_t)tile * (size_t)g.tile_words;
 
+    // ---- A: stage the rows.  Row r is issued by lane r / 6 of warp r % 6 (a bulk copy is a
+    // uniform-datapath instruction, so a warp issues its copies one after the other: 11 per warp
+    // instead of 32).  Memory safety of the copy does not depend on the caller's batch arrays.
+    if (lane * (NT / 32) + wid < T) {
+        const int r = lane * (NT / 32) + wid;
+        const int rb = tile * T + r;
+        const int rbegin = first + rb * bs;
+        int rn = has_tile && rb < c.n_batches ? min(bs, last_end - rbegin) : 0;
+        if (rn != 0 && (first < 0 || (first & 3) || rn < 0 || (int64_t)rbegin + rn > c.n_idx || rn % 3 != 0 || rn > c.max_span)) rn = 0;  // reported by the row's dedup thread
+        const uint32_t dst = sbase + row_bytes * (uint32_t)r + 4u * (uint32_t)g.slack;
+        const uint32_t bytes = (rn & 3) == 0 ? 4u * (uint32_t)rn : 0u;
+        if (!bytes) {
+#pragma unroll 1
+            for (int i = 0; i < rn; i++) sts_u32(dst + 4 * i, __ldg(c.idx + rbegin + i));  // short last batch
+        }
+        mbar_arrive_expect_tx(bar, bytes);
+        if (bytes) bulk_g2s(dst, c.idx + rbegin, bytes, bar);
+    }
+
     if (dedup_thread) {
         const int b = tile * T + t;
         bool active = has_tile && b < c.n_batches;
@@ -366,16 +388,6 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         }
         const int claimed_begin = active ? __ldg(c.bbegin + b) : 0, claimed_end = active ? __ldg(c.bend + b) : 0;
 
-        // ---- A: stage the row
-        {
-            const uint32_t bytes = (n & 3) == 0 ? 4u * (uint32_t)n : 0u;
-            if (!bytes) {
-#pragma unroll 1
-                for (int i = 0; i < n; i++) sts_u32(a_ids + 4 * i, __ldg(c.idx + begin + i));  // short last batch
-            }
-            mbar_arrive_expect_tx(bar, bytes);
-            if (bytes) bulk_g2s(a_ids, c.idx + begin, bytes, bar);
-        }
         mbar_wait(bar, 0);
         VR_MARK(2);
 
