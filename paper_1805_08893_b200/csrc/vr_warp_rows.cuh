@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const bool live = p < n;
-                const uint32_t xk = (x << 8) | tagw;
+                const uint32_t xk = x * 256u + tagw;              // id << 8 | tag: one IMAD
                 const uint32_t tq = v ^ xk;                       // == rank (< W) iff the slot holds x in this round
                 const bool hit = tq < (uint32_t)W;
                 const bool fre = (tq & kTagMask) != 0;            // slot not used in this round
