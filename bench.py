@@ -314,17 +314,18 @@ def main():
         peak, peak_src = (peaks["hbm_gbs"], "measured (MEASURED_PEAKS.json hbm_gbs)") if "hbm_gbs" in peaks \
             else (6650.0, "fallback (B200_PROFILING.md)")
         launches = lib.vr_last_launch_count()
-        fused = launches in (2, 3)  # init + one kernel that dedups, places and shades (+ its drain kernel)
+        path = lib.vr_last_kernel_path()
+        fused = path >= 2  # init + one kernel that dedups, places and shades
         dom = int(np.argmax(stage_ms))
         # per-kernel algorithmic bytes: dedup = index read + map write + metadata;
         # shade/finalize = staged id read is not algorithmic: position read + shaded write
         kernel_alg = {"dedup": 4 * n_idx + 2 * n_idx + 12 * nb, "shade_finalize": 32 * inv}
-        dom_name = ("tile kernel (stage + dedup + decoupled look-back/shade) + its drain kernel" if launches == 3
+        dom_name = ("persistent tile kernel (stage + dedup + decoupled look-back/shade)" if path == 3
                     else "fused dedup+offsets+shade" if fused else N.PROFILE_STAGE_NAMES[dom])
         traffic = None  # DRAM bytes per step of the dominant kernel(s), from the committed ncu --set full capture
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
-            if tj.get("workload") == name and launches == 3:
+            if tj.get("workload") == name and path == 3:
                 traffic = tj["traffic_bytes_per_step"]
         except Exception:
             pass

@@ -202,6 +202,10 @@ int vr_profile_enable(int on);
 /* Number of kernels the last vr_run of this process launched (bench.py's gpu_launches). */
 int vr_last_launch_count(void);
 int vr_profile_read(float *ms, int cap);
+/* Which dedup path the last vr_run of this process took (tests and bench.py report it):
+ * 0 = generic kernels (K1 -> K2 -> K3), 1 = static-batch warp kernel (unfused), 2 = static-batch warp
+ * kernel with fused look-back + shading, 3 = persistent tile kernel (csrc/vr_warp_rows.cuh). */
+int vr_last_kernel_path(void);
 
 #ifdef __cplusplus
 }

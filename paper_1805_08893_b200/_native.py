@@ -78,6 +78,7 @@ _SIGNATURES = {
                          C.POINTER(OutputsC), C.c_void_p, C.c_size_t, C.c_void_p]),
     "vr_profile_enable": (C.c_int, [C.c_int]),
     "vr_last_launch_count": (C.c_int, []),
+    "vr_last_kernel_path": (C.c_int, []),
     "vr_profile_read": (C.c_int, [C.POINTER(C.c_float), C.c_int]),
     "vr_expand_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,

@@ -1380,6 +1380,7 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
 static cudaEvent_t g_prof_ev[VR_PROFILE_STAGES + 1];
 static int g_prof_on = 0, g_prof_marks = 0;
 static int g_last_launches = 0;  // kernels launched by the last vr_run of this process
+static int g_last_path = 0;      // see vr_last_kernel_path()
 static inline void prof_mark(cudaStream_t s) {
     if (g_prof_on && g_prof_marks <= VR_PROFILE_STAGES) cudaEventRecord(g_prof_ev[g_prof_marks++], s);
 }
@@ -1621,6 +1622,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
                       shader->vertex_count <= (1 << 24);
     c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : 0;
     g_prof_marks = 0;
+    g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : 0;
     prof_mark(stream);
     init_kernel<<<(int)ceil_div(c.n_fused_tiles + ACC_WORDS, 256), 256, 0, stream>>>(c);
     if (!contiguous && nb > 0) span_scan_kernel<<<1, 1024, 0, stream>>>(c);
@@ -1680,7 +1682,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (fused) {
         prof_mark(stream);
         prof_mark(stream);
-        g_last_launches = rows ? 3 : 2;  // init + tile kernel (+ drain kernel)
+        g_last_launches = 2;  // init + one kernel that dedups, places and shades
         VR_CUDA_CHECK(cudaGetLastError());
         return VR_OK;
     }
@@ -1707,6 +1709,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
 }
 
 int vr_last_launch_count(void) { return g_last_launches; }
+int vr_last_kernel_path(void) { return g_last_path; }
 
 #ifdef VR_TIMELINE
 // debugging aid (not part of the ABI): copies the phase time stamps of the last tile-kernel launch

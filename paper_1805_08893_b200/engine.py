@@ -157,6 +157,7 @@ class DeviceRun:
         self.shade_counts = None
         self.stats_dev = None
         self.launches = 0
+        self.kernel_path = 0
         self._stats = None
 
     # -- statistics -----------------------------------------------------------------
@@ -318,5 +319,6 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                         ws.numel(), _stream_ptr())
     raise_status(st)
     run.launches = lib.vr_last_launch_count()  # kernels this call launched (bench.py's gpu_launches)
+    run.kernel_path = lib.vr_last_kernel_path()  # 3 = persistent tile kernel (include/vrgeom.h)
     run._keep = (ws, shader)
     return run

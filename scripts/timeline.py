@@ -43,17 +43,17 @@ def stat(name, d):
     d = d.reshape(-1) / 1e3
     print(f"  {name:28s} median {np.median(d):7.2f}  p10 {np.percentile(d, 10):7.2f}  p90 {np.percentile(d, 90):7.2f}  mean {d.mean():7.2f} us")
 d = a[:, 0, :nt]
-print(f"tiles {nt}; dedup warp 0 (CTAs that own a tile); span to last publish {(d[5].max() - t0) / 1e3:.1f} us")
-for k, nm in enumerate(["entry->ticket", "ticket->staged", "dedup", "wait for helpers", "post (indices, scratch, publish)"]):
+t0 = d[1].min()
+print(f"tiles {nt}; dedup warp 0 (iterations of the persistent CTAs that own a tile); span to last publish {(d[5].max() - t0) / 1e3:.1f} us")
+for k, nm in ((1, "ticket -> rows staged (wait)"), (2, "dedup"), (3, "barrier"), (4, "post (scratch, next staging, indices, publish)")):
     stat(nm, d[k + 1] - d[k])
-stat("lifetime", d[5] - d[0])
+stat("iteration", d[5] - d[1])
 h = a[:, 1, :]
-sel = np.arange(592, nt)  # CTAs whose helpers shade a tile and check a tile
-print("helper warp 2")
-stat("range check", h[7, sel] - h[1, sel])
+lag = int(os.environ.get("VR_LAG", 888))
+sel = np.arange(lag, nt)  # iterations whose helpers shade a tile
+print("helper warp 2 (shading tile i - K)")
 stat("look-back + shading", h[6, sel] - h[7, sel])
-stat("  wait aggregate + fence", h[8, sel] - h[7, sel])
+stat("  wait aggregate", h[8, sel] - h[7, sel])
 stat("  ids, gathers, look-back", h[9, sel] - h[8, sel])
 stat("  stores + further steps", h[10, sel] - h[9, sel])
 stat("  round tables", h[6, sel] - h[10, sel])
-print("tile start times (us) at tile 0, 592, 1184, ...:", [round(float((d[0, i] - t0) / 1e3), 1) for i in range(0, nt, 592)])

@@ -35,7 +35,7 @@ def tile_run(idx, cfg, spec, counts=False, lag=None):
         os.environ.pop("VR_LAG", None)
         if old is not None:
             os.environ["VR_LAG"] = old
-    assert run.launches == 3, "expected init + tile kernel + drain kernel"
+    assert run.kernel_path == 3 and run.launches == 2, "expected init + the persistent tile kernel"
     return run, so
 
 
