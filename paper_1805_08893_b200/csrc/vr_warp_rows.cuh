@@ -161,7 +161,14 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
     const bool want_uid = c.out.d_unique_ids != nullptr;
     const bool want_pos = sp.kind == VR_SHADER_POSITION;
     uint32_t m0 = 0, m1 = 0;  // round-table metadata of row ht, in flight with everything else
-    if (ht < T) { m0 = __ldcg(sc + ht); m1 = __ldcg(sc + T + ht); }
+    constexpr int RW = 4;     // round records fetched up front (a 96-index batch at W = 32 has at most 4 rounds)
+    uint32_t rw[RW];
+    if (ht < T) {
+        m0 = __ldcg(sc + ht);
+        m1 = __ldcg(sc + T + ht);
+#pragma unroll
+        for (int q = 0; q < RW; q++) rw[q] = q < g.max_rounds ? __ldcg(sc + 2 * T + q * T + ht) : 0u;
+    }
     // ---- E (part 1): the first U8 claims of every thread are gathered and shaded while the
     // first helper warp is still resolving the tile's output offsets
     constexpr int U8 = 8;
@@ -285,8 +292,16 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
                 const int r0w = off.x + (int)(m1 & 0xFFFFu);
                 int run = off.y + (int)(m0 & 0xFFFFu);
                 if (c.out.d_batch_round_off) c.out.d_batch_round_off[sb] = r0w;
+#pragma unroll
+                for (int q = 0; q < RW; q++) {
+                    if (q < nr) {
+                        if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0w + q] = run;
+                        if (c.out.d_round_prims) c.out.d_round_prims[r0w + q] = (int)(rw[q] >> 8);
+                        run += (int)(rw[q] & 0xFFu);
+                    }
+                }
 #pragma unroll 1
-                for (int q = 0; q < nr; q++) {
+                for (int q = RW; q < nr; q++) {
                     const uint32_t wv = __ldcg(sc + 2 * T + q * T + ht);
                     if (c.out.d_round_uid_off) c.out.d_round_uid_off[r0w + q] = run;
                     if (c.out.d_round_prims) c.out.d_round_prims[r0w + q] = (int)(wv >> 8);
