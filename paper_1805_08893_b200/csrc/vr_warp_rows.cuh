@@ -2,32 +2,34 @@
 // Included by vr_run.cu inside namespace vr (uses RunCtx, report_error, finish_stats, lds_*/sts_*).
 //
 // A TILE is 64 consecutive static batches (batching.py:76-84): one contiguous 64 * batch_size *
-// 4-byte piece of the index buffer.  A CTA has 2 dedup warps (one thread per batch) and 4 helper
-// warps, and works on TWO tiles at once -- software pipelining across tiles:
+// 4-byte piece of the index buffer.  The grid is PERSISTENT (one CTA per shared-memory slot of the
+// GPU, 4 per SM); a CTA has 2 dedup warps (one thread per batch) and 4 helper warps and draws
+// tickets in a loop.  With ticket i it works on TWO tiles at once -- software pipelining across tiles:
 //
-//   dedup warps, tile i (ticket order)
+//   dedup warps, tile i
 //     A  stage   every row (batch) arrives by ONE bulk asynchronous copy (cp.async.bulk, the 1-D
 //                TMA path, completion on an mbarrier) into its own shared-memory row: the tile is
-//                read from HBM as whole 128-byte lines, no register staging.
+//                read from HBM as whole 128-byte lines, no register staging.  The copies of tile
+//                i were issued during the post phase of the CTA's previous tile.
 //     B  dedup   one THREAD per batch runs the closed form of Algorithm 1 over its row as a
 //                per-lane state machine (see below).  Claims are appended IN PLACE at the front of
 //                the row, local indices are bytes in a rank row.
-//     C  post    all six warps: local indices leave as coalesced 16-byte stores (8 x uint16); the
-//                rows' claims are copied, compacted, into the tile's slot of an L2-resident
-//                scratch list together with the per-row round records; then the tile's
-//                (rounds, claims) AGGREGATE is published and the CTA is done -- it never waits
-//                for its output offsets, its shared memory is free for the next tile.
-//   helper warps, tile j = i - K  (K = CTAs resident on the GPU: tile j is complete by then)
+//     C  post    all six warps: the rows' claims are copied, compacted, into the tile's slot of an
+//                L2-resident scratch list together with the per-row round records; the next
+//                ticket's rows are staged; local indices leave as coalesced 16-byte stores
+//                (8 x uint16); then the tile's (rounds, claims) AGGREGATE is published.  The CTA
+//                never waits for the tile's output offsets.
+//   helper warps, tile j = i - K  (K = 1.5 x the number of CTAs: tile j was published half a round ago)
 //     D  offsets decoupled look-back over the published aggregates (no waiting in the steady
-//                state: every predecessor of j finished long ago); publishes j's inclusive prefix;
+//                state); publishes j's inclusive prefix;
 //     E  shade   the tile's flat claim list is streamed from the scratch (L2 hits): coalesced id
 //                store, 16-byte position gather, FP32 4x4 transform + w-divide (strategies.py:53-67),
 //                coalesced 16-byte stores; round tables from the round records.
 //                This memory-bound work runs UNDER the compute-bound dedup of tile i.
-//     F  check   every index of tile i is range-checked against the vertex count and its vertex
-//                prefetched into L2 (it is gathered ~K tiles later).
+//     F  (optional, VR_PREFETCH=1) the vertices of tile i are prefetched into L2.
 //
-// The last K tiles are shaded by a light second kernel (rows_drain_kernel).
+// The K tickets after the last tile only shade (their dedup warps idle).
+// Debug / tuning knobs (environment, read at launch): VR_LAG=<K>, VR_PREFETCH=1, VR_NO_PDL=1.
 #pragma once
 
 constexpr int kRowThreads = 64;      // batches per tile = dedup threads
@@ -128,7 +130,7 @@ __device__ __forceinline__ unsigned long long timeline_now() {
 #endif
 
 // ---- D/E: shading of one finished tile by 128 threads (4 warps; `ht` = 0..127).  Used by the helper
-// warps of the tile kernel (tile = ticket - K) and by the drain kernel (the last K tiles).
+// warps of the tile kernel (tile = ticket - K).
 template <int DUMMY>
 __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom& g, const ShaderParams& sp, int stile, int ht,
                                                 int2* s_base_ptr) {
