@@ -41,6 +41,9 @@ WORKLOADS = {
     "c4_hash": dict(desc="configs[3]: shuffle_triangles(gen_grid(1898,1898), 0), dynamic 256/1023, hash 256",
                     side=1898, shuffle=0, strategy="hash", batching="dynamic",
                     expect=dict(batches=84672, rounds=84672, invocations=21591005, probes_fast=216377586)),
+    "c4_phash": dict(desc="configs[3] mesh, dynamic 256/1023, two-tier hash 256 (exactness row, lane 0 replays the reference)",
+                     side=1898, shuffle=0, strategy="phash", batching="dynamic",
+                     expect=dict(batches=84672, rounds=84672, invocations=21591005)),
     "c4_sort": dict(desc="configs[3] mesh, dynamic 256/1023, sort dedup",
                     side=1898, shuffle=0, strategy="sort", batching="dynamic",
                     expect=dict(batches=84672, rounds=84672, invocations=21591005)),

@@ -1048,6 +1048,126 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
 }
 
 // ---------------------------------------------------------------------------------
+// K1 (phash): strategies.py:301-367 -- two-tier hashing.  The reference is a sequential emulation
+// whose table layout and probe statistics depend on the exact order of events: per group of
+// warp_width slots every element probes at most max_fast_probes slots of a table that already
+// holds the group's earlier insertions, then the deferred elements are inserted one at a time by
+// scanning warp_width-slot windows.  One WARP per batch: the batch, the table and the slot map
+// live in shared memory, lane 0 replays the reference's order of events literally (exactness
+// first: SURVEY.md 8f-1), all lanes stage the batch and produce the outputs (occupied slots
+// ranked in table order, strategies.py:370-380).
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, int w, int mfp, int per_warp_bytes) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int warps = blockDim.x >> 5;
+    const int b = blockIdx.x * warps + wid;
+    if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
+    const uint32_t tsize = c.table_size;
+    unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
+    uint32_t* ids = reinterpret_cast<uint32_t*>(base);
+    uint32_t* tab = ids + n_max;                                        // [tsize] ids
+    int32_t* d_i = reinterpret_cast<int32_t*>(tab + tsize);             // deferred elements of a group: index,
+    int32_t* d_p = d_i + 64;                                            //   slot where fast probing stopped,
+    int32_t* d_chain = d_p + 64;                                        //   probes so far
+    uint16_t* slot_map = reinterpret_cast<uint16_t*>(d_chain + 64);     // [n_max]
+    uint16_t* rank_of = slot_map + n_max;                               // [tsize]
+    uint8_t* occ = reinterpret_cast<uint8_t*>(rank_of + tsize);         // [tsize]
+    int begin, n;
+    if (!validate_batch(c, b, begin, n)) {
+        if (lane == 0) c.counts[b] = make_int2(0, 0);
+        return;
+    }
+    const int mo = batch_map_off(c, b, begin);
+    for (int i = lane; i < n; i += 32) ids[i] = __ldg(c.idx + begin + i);
+    for (int s = lane; s < (int)tsize; s += 32) occ[s] = 0;
+    __syncwarp();
+    int status = VR_OK;
+    long long fast = 0, slow = 0;
+    int max_chain = 0;
+    if (lane == 0) {
+        for (int gb = 0; gb < n && status == VR_OK; gb += w) {  // strategies.py:321
+            int nd = 0;
+            const int top = min(gb + w, n);
+            for (int i = gb; i < top; i++) {
+                const uint32_t vid = ids[i];
+                uint32_t p = hash_slot(vid, c.multiplier, c.table_bits);
+                int chain = 0, resolved = -1;
+                while (chain < mfp) {  // :328
+                    chain++;
+                    if (!occ[p]) { occ[p] = 1; tab[p] = vid; resolved = (int)p; break; }
+                    if (tab[p] == vid) { resolved = (int)p; break; }
+                    p = p + 1 == tsize ? 0 : p + 1;
+                }
+                fast += chain;
+                if (resolved >= 0) {
+                    slot_map[i] = (uint16_t)resolved;
+                    max_chain = max(max_chain, chain);
+                } else {
+                    d_i[nd] = i; d_p[nd] = (int)p; d_chain[nd] = chain; nd++;
+                }
+            }
+            for (int d = 0; d < nd && status == VR_OK; d++) {  // :345
+                const int i = d_i[d];
+                uint32_t p = (uint32_t)d_p[d];
+                int chain = d_chain[d];
+                const uint32_t vid = ids[i];
+                long long scanned = 0;
+                for (;;) {
+                    if (scanned > (long long)tsize + w) { status = VR_ERR_HASH_FULL; break; }  // :348-349
+                    slow += w;  // :351
+                    int pos = 0;
+                    for (int l = 0; l < w; l++) {  // ballot + ffs over the window
+                        const uint32_t sl = (p + (uint32_t)l) % tsize;
+                        if (!occ[sl] || tab[sl] == vid) { pos = l + 1; break; }
+                    }
+                    if (pos) {
+                        const uint32_t sl = (p + (uint32_t)(pos - 1)) % tsize;
+                        if (!occ[sl]) { occ[sl] = 1; tab[sl] = vid; }
+                        slot_map[i] = (uint16_t)sl;
+                        max_chain = max(max_chain, chain + pos);
+                        break;
+                    }
+                    p = (p + (uint32_t)w) % tsize;
+                    chain += w;
+                    scanned += w;
+                }
+            }
+        }
+    }
+    status = __shfl_sync(0xffffffffu, status, 0);
+    __syncwarp();
+    if (status != VR_OK) {
+        if (lane == 0) { report_error(c, b, status); c.counts[b] = make_int2(0, 0); }
+        return;
+    }
+    // occupied slots ranked in table order, unique ids, local indices
+    uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
+    int run = 0;
+    for (int s0 = 0; s0 < (int)tsize; s0 += 32) {
+        const int s = s0 + lane;
+        const bool o = s < (int)tsize && occ[s];
+        const uint32_t m = __ballot_sync(0xffffffffu, o);
+        if (o) {
+            const int rk = run + __popc(m & ((1u << lane) - 1));
+            rank_of[s] = (uint16_t)rk;
+            suid[rk] = tab[s];
+        }
+        run += __popc(m);
+    }
+    __syncwarp();
+    if (c.out.d_assembly_map)
+        for (int i = lane; i < n; i += 32) c.out.d_assembly_map[mo + i] = rank_of[slot_map[i]];
+    if (lane == 0) {
+        c.counts[b] = make_int2(1, run);
+        atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], (unsigned long long)fast);
+        atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_SLOW], (unsigned long long)slow);
+        atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)max_chain);
+        if (c.enforce_budget && run > c.max_unique) report_error(c, b, VR_ERR_OVER_BUDGET);
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // K2: exclusive scan of per-segment (rounds, invocations).  Up to 32768 segments one CTA
 // does it all; beyond that, 1024-segment tiles are reduced, the tile sums scanned by the
 // same single-CTA kernel, and a down-sweep writes the per-segment offsets.
@@ -1551,7 +1671,6 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         if (st) return st;
         if (!no_budget && (int64_t)hc.table_size < cfg->max_unique) return VR_ERR_TABLE_BELOW_BUDGET;  // strategies.py:432-435
     }
-    if (strategy == VR_PHASH) return VR_ERR_UNSUPPORTED;
     if (n_idx > 0x7fffffffLL || nb > 0x7fffffffLL || span_total > 0x7fffffffLL || n_idx < 0 || nb < 0 || span_total < 0)
         return VR_ERR_UNSUPPORTED;
     if (strategy == VR_WARP && nb > 0 && cfg->warp_width < cfg->primitive_size) return VR_ERR_WARP_WIDTH;
@@ -1604,6 +1723,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         pmax = (int)next_pow2((uint32_t)(max_span < 2 ? 2 : max_span));
         smem = (size_t)pmax * (8 + 4 + 2);
         VR_CUDA_CHECK(cudaFuncSetAttribute(sort_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    } else if (strategy == VR_PHASH && nb > 0) {
+        if (max_span > 65535 || hc.table_size > 65536) return VR_ERR_UNSUPPORTED;  // 16-bit slot map / ranks
     } else if (strategy == VR_HASH && nb > 0) {
         nmax = (max_span + 3) & ~3;
         q = (int)next_pow2((uint32_t)(2 * nmax < 64 ? 64 : 2 * nmax));
@@ -1659,6 +1780,15 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             default: st = launch_warp_tpb<64>(c, stream); break;
             }
             if (st) return st;
+        } else if (strategy == VR_PHASH) {
+            const int wn = (max_span + 3) & ~3;
+            const int per_warp = (wn * 4 + (int)hc.table_size * 4 + 3 * 64 * 4 + wn * 2 + (int)hc.table_size * 2 + (int)hc.table_size + 15) & ~15;
+            if (per_warp > 200 * 1024) return VR_ERR_UNSUPPORTED;
+            int warps = 8;
+            while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
+            const size_t wsmem = (size_t)warps * per_warp;
+            VR_CUDA_CHECK(cudaFuncSetAttribute(phash_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+            phash_warp_kernel<<<(int)ceil_div(nb, warps), warps * 32, wsmem, stream>>>(c, wn, cfg->warp_width, (int)hc.max_fast_probes, per_warp);
         } else if (strategy == VR_SORT) {
             sort_batch_kernel<<<nbi, 256, smem, stream>>>(c, pmax);
         } else {

@@ -255,8 +255,17 @@ def hash_batch(ids, hash_cfg: HashConfig, primitive_size: int = 3):
 
 
 def parallel_hash_batch(ids, hash_cfg: HashConfig, warp_width: int, primitive_size: int = 3):
-    """Two-tier hashing (strategies.py:301-367): SURVEY.md 8(f-1), not built on the device yet."""
-    raise UnsupportedOnDevice("phash is not available on the device path yet (SURVEY.md 8f-1)")
+    """Two-tier hashing (strategies.py:301-367): same stream and invocation count as hash_batch, its own
+    table layout and probe statistics (fast / slow)."""
+    w = check_width(warp_width)
+    if len(ids) == 0:
+        return DedupResult((Round((), (), 0),), 0, 0), ProbeStats()
+    n = len(ids)
+    size = max(primitive_size, n)
+    cfg = BatchConfig(batch_size=size, max_unique=size, max_indices=size, warp_width=w, primitive_size=primitive_size)
+    run, flat = _single_batch("phash", ids, cfg, hash_cfg)
+    fast, slow, mx = run.probes
+    return _result_from_flat(flat, primitive_size), ProbeStats(fast=fast, slow=slow, max_chain=mx)
 
 
 # ---------------------------------------------------------------------------
@@ -339,8 +348,6 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
                 f"hash table_size {hash_cfg.table_size} below max_unique {cfg.max_unique}")
     if strategy == "warp" and nb and cfg.warp_width < ps:
         raise ConfigError("warp width below primitive size cannot make progress")
-    if strategy == "phash" and nb:
-        raise UnsupportedOnDevice("phash is not available on the device path yet (SURVEY.md 8f-1)")
 
     probe_total = ProbeStats() if strategy in ("hash", "phash") else None
     if nb == 0:  # strategies.py:472-502 with an empty result list

@@ -39,7 +39,7 @@ def check_against_oracle(strategy, idx, offs, cfg, hcfg=None, ctx=""):
     fr = oracle_run(strategy, idx, offs, cfg, hcfg)
     assert_flat_equal(run.flat(), oracle_flat(fr), f"{ctx} {strategy}")
     assert (run.invocations, run.rounds, run.indices) == (fr.invocations, fr.rounds, fr.indices)
-    if strategy == "hash":
+    if strategy in ("hash", "phash"):
         assert run.probes == (fr.probes_fast, fr.probes_slow, fr.probe_max_chain), ctx
     return run, fr
 
@@ -71,6 +71,22 @@ def test_reference_kats(cuda_lib):
     assert r.invocations == 6 and len(r.rounds) == 2 and r.rounds[1].unique_ids == (0, 2, 3)
 
 
+def test_phash_engineered_collisions(cuda_lib):
+    """Reference tests/test_strategies.py:170-181: ids that all collide in a table of 8 force the
+    warp-cooperative slow path; same corner stream as hash_batch, slow probes recorded."""
+    ids = np.repeat(np.array([0, 5, 13, 18, 26, 34], dtype=np.uint32), 3)
+    hc = HashConfig(table_size=8, max_fast_probes=2)
+    rp, sp = P.parallel_hash_batch(ids, hc, 4)
+    rh, _ = P.hash_batch(ids, hc)
+    want_rounds, inv, _, probes = O.parallel_hash_batch(ids, 4, table_size=8, max_fast_probes=2)
+    assert (sp.fast, sp.slow, sp.max_chain) == tuple(probes) and sp.slow > 0 and rp.invocations == inv == 6
+    assert [tuple(r.unique_ids) for r in rp.rounds] == [tuple(int(v) for v in r[0]) for r in want_rounds]
+    corners = lambda res: [r.unique_ids[s] for r in res.rounds for s in r.assembly_map]
+    assert corners(rp) == corners(rh) == ids.tolist()
+    with pytest.raises(RuntimeError):  # more unique ids than slots (strategies.py:348-349)
+        P.parallel_hash_batch(np.arange(9, dtype=np.uint32).repeat(3)[:27], HashConfig(table_size=8), 4)
+
+
 def test_kernels_golden(cuda_lib):
     data, meta = load_npz("kernels.npz"), load_json("kernels.json")
     for case in meta:
@@ -78,14 +94,14 @@ def test_kernels_golden(cuda_lib):
         ids = data[f"k{k}_ids"]
         n = len(ids)
         cfg = BatchConfig(batch_size=n, max_unique=max(n, 3), max_indices=n, warp_width=case["warp_width"])
-        hc = HashConfig(table_size=case["table_size"])
-        for strat in ("naive", "warp", "sort", "hash"):
+        hc = HashConfig(table_size=case["table_size"], max_fast_probes=case["max_fast_probes"])
+        for strat in ("naive", "warp", "sort", "hash", "phash"):
             run = engine.run_device(strat, engine.to_device_indices(ids), *_one(ids), 1, n, n, cfg, hc,
                                     engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY), enforce_budget=False)
             want = {name: data[f"k{k}_{strat}_{name}"] for name in FLAT_KEYS}
             assert_flat_equal(run.flat(), want, f"case {k} w={case['warp_width']} {strat}")
-            if strat == "hash":
-                assert list(run.probes) == case[strat]["probes"], f"case {k} probes"
+            if strat in ("hash", "phash"):
+                assert list(run.probes) == case[strat]["probes"], f"case {k} {strat} probes"
 
 
 def _one(ids):
@@ -105,7 +121,7 @@ def test_runs_golden(cuda_lib):
         stat = P.static_batches(len(mesh.indices), cfg)
         dyn = P.dynamic_batches(mesh.indices, cfg)
         assert np.array_equal(P.batches_to_offsets(dyn), data[f"m{i}_dynamic"]), f"mesh {i} dynamic"
-        for strat, batches in (("naive", stat), ("warp", stat), ("sort", dyn), ("hash", dyn)):
+        for strat, batches in (("naive", stat), ("warp", stat), ("sort", dyn), ("hash", dyn), ("phash", dyn)):
             out = P.run_on_indices(strat, mesh.indices, batches, cfg, P.position_shader(mesh, MATRIX), hc,
                                    vertex_count=mesh.vertex_count, scene=f"m{i}")
             stream, rep = out[0], out[1]
@@ -151,12 +167,12 @@ def test_random_batches_vs_oracle(cuda_lib):
         offs = np.concatenate([[0], np.cumsum([len(x) for x in ids_list])]).astype(np.int64)
         span = int(np.diff(offs).max())
         for strat, w in (("naive", 32), ("warp", 32), ("warp", 4), ("warp", 8), ("warp", 16), ("warp", 64),
-                         ("sort", 32), ("hash", 32)):
+                         ("sort", 32), ("hash", 32), ("phash", 32), ("phash", 8)):
             cfg = BatchConfig(batch_size=span, max_unique=mu, max_indices=span, warp_width=w,
                               block_size=next_pow2(mu))
             run, fr = check_against_oracle(strat, idx, offs, cfg, HashConfig(table_size=next_pow2(mu)),
                                            ctx=f"seed {seed} w={w}")
-            if strat in ("sort", "hash"):
+            if strat in ("sort", "hash", "phash"):
                 assert fr.invocations == sum(len(set(x.tolist())) for x in ids_list)
 
 

@@ -106,7 +106,7 @@ def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
     assert h[0] == 0 and h[-1] == len(mesh.indices) and (np.diff(h) > 0).all() and (np.diff(h) % 3 == 0).all()
     k = 3000
     assert np.array_equal(h[:k], O.dynamic_batches(mesh.indices[:int(h[k])])[:k])
-    for strat in ("hash", "sort"):
+    for strat in ("hash", "sort", "phash"):
         run = engine.run_device(strat, d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 1023, cfg,
                                 HashConfig(), engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY)).check()
         assert run.invocations == 21591005
@@ -118,3 +118,5 @@ def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
         sub = engine.run_device(strat, d_idx, offs[:k], offs[1:k + 1], k, int(sub_offs[-1]), 1023, cfg,
                                 HashConfig(), engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
         assert_flat_equal(sub.flat(), oracle_flat(fr), f"config4 {strat} prefix")
+        if strat in ("hash", "phash"):
+            assert sub.probes == (fr.probes_fast, fr.probes_slow, fr.probe_max_chain)
