@@ -36,7 +36,7 @@ struct DynCtx {
     int cap;      // max primitives per batch (batching.py:58-61)
     int window;   // ps * cap positions
     int tile;     // positions per A1 tile (multiple of 32)
-    int slots;    // A1 table slots (power of two)
+    int slots;    // A1 table slots (any multiple of 32)
     int chunk;    // primitives per chunk, >= cap
     int n_chunks;
     int n_groups;
@@ -61,15 +61,19 @@ __global__ void fill_kernel(int32_t* p, int n, int v) {
 }
 
 // ---- A1 -----------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_tiles) {
+// One warp per tile of positions, preceded by a halo of one batch window.  The table (open addressing,
+// no deletions) holds every distinct id of tile + halo: `slots` is NOT a power of two (multiply-high
+// hash), sized for a load of 0.8, and the last position of an id is kept relative to the halo start
+// in 16 bits -- 6 bytes per slot instead of 16, which is what decides how many warps an SM can hold.
+template <typename LastT>
+__global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_tiles, int per_warp_bytes) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int tile_id = blockIdx.x * (blockDim.x >> 5) + wid;
-    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw) + (size_t)wid * 2 * c.slots;
-    int32_t* last = reinterpret_cast<int32_t*>(keys + c.slots);
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw + (size_t)wid * per_warp_bytes);
+    LastT* last = reinterpret_cast<LastT*>(keys + c.slots);
     if (tile_id >= n_tiles) return;
-    const uint32_t mask = (uint32_t)c.slots - 1;
-    const int sbits = ilog2((uint32_t)c.slots);
+    const uint32_t nslots = (uint32_t)c.slots;
     for (int i = lane; i < c.slots; i += 32) keys[i] = kEmpty;
     __syncwarp();
     const int t0 = tile_id * c.tile;
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_t
         const uint32_t lower = peers & lt;
         const bool leader = valid && lower == 0;
         const int hipeer = 31 - __clz(peers);
-        uint32_t h = (id * 0x9E3779B1u) >> (32 - sbits);
+        uint32_t h = __umulhi(id * 0x9E3779B1u, nslots);
         bool active = leader, existed = false;
         while (__any_sync(0xffffffffu, active)) {
             uint32_t k = active ? keys[h] : 0u;
@@ -94,16 +98,16 @@ __global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_t
             if (claim) keys[h] = id;
             __syncwarp();
             if (claim) {
-                if (keys[h] == id) active = false; else h = (h + 1) & mask;
+                if (keys[h] == id) active = false; else h = h + 1 == nslots ? 0u : h + 1;
             } else if (active) {
-                h = (h + 1) & mask;
+                h = h + 1 == nslots ? 0u : h + 1;
             }
             __syncwarp();
         }
         int pv = -1;
         if (leader) {
-            if (existed) pv = last[h];
-            last[h] = base + hipeer;
+            if (existed) pv = hs + (int)last[h];
+            last[h] = (LastT)(base + hipeer - hs);
         } else if (valid) {
             pv = base + (31 - __clz(lower));
         }
@@ -235,13 +239,11 @@ static DynLayout dyn_layout(int64_t n, const vr_batch_config* cfg) {
     L.n_chunks = (int)ceil_div(L.T > 0 ? L.T : 1, L.chunk);
     L.n_groups = (int)ceil_div(L.n_chunks, kGroup);
     int tile = (L.window + 31) & ~31;
-    if (tile < 1024) tile = 1024;
+    if (tile < 1024) tile = 1024;  // (2048 halves the halo overhead but also the warps per SM: measured slower)
     L.tile = tile;
-    {   // distinct ids seen by one warp <= tile + halo; keep the table load below ~0.67
+    {   // distinct ids seen by one warp <= tile + halo
         const int cnt = tile + ((L.window + 31) & ~31) + 32;
-        int slots = (int)next_pow2((uint32_t)cnt);
-        if (2 * slots < 3 * cnt) slots <<= 1;
-        L.slots = slots;
+        L.slots = ((cnt + cnt / 4) + 31) & ~31;  // load <= 0.8
     }
     size_t o = 0;
     L.prev = o; o += al((size_t)n * 4 + 64);
@@ -284,10 +286,13 @@ int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* 
     }
     DynLayout L = dyn_layout(n, cfg);
     if (!d_ws || ws_bytes < L.total) return VR_ERR_WORKSPACE;
-    const int warps_per_cta = 4;
-    size_t smem = (size_t)warps_per_cta * L.slots * 8;
-    int wpc = warps_per_cta;
-    while (smem > 200 * 1024 && wpc > 1) { wpc >>= 1; smem = (size_t)wpc * L.slots * 8; }
+    // link table: 4-byte key + last position of the id relative to the halo start (16 bits when the
+    // tile and its halo span fewer than 65 536 positions)
+    const bool small_last = (int64_t)L.tile + L.window + 64 < 65536;
+    const int per_warp = (L.slots * (small_last ? 6 : 8) + 15) & ~15;
+    int wpc = 4;
+    while ((size_t)wpc * per_warp > 200 * 1024 && wpc > 1) wpc >>= 1;
+    const size_t smem = (size_t)wpc * per_warp;
     if (smem > 200 * 1024) return VR_ERR_UNSUPPORTED;  // batch window too long for the link table
     unsigned char* ws = (unsigned char*)d_ws;
     DynCtx c{};
@@ -303,8 +308,13 @@ int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* 
 
     fill_kernel<<<(int)ceil_div(n, 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
     const int n_tiles = (int)ceil_div(n, L.tile);
-    VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    occurrence_links_kernel<<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles);
+    if (small_last) {
+        VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        occurrence_links_kernel<uint16_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
+    } else {
+        VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        occurrence_links_kernel<int32_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
+    }
     const int run = 64;
     const int n_threads = (int)ceil_div(L.T, run);
     greedy_next_kernel<<<(int)ceil_div(n_threads, 128), 128, 0, stream>>>(c, run);
