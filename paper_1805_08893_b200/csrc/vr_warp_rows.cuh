@@ -54,7 +54,7 @@ static inline bool rows_geometry(int W, int bs, RowsGeom& g) {
     const int per_round = 3 * (W / 3);
     g.max_rounds = (bs + per_round - 1) / per_round;
     g.slack = (2 * g.max_rounds + 2) & ~3;  // >= 2 * max_rounds - 1: see the claim-list store in the dedup loop
-    int rw = bs + g.slack;
+    int rw = bs + g.slack + 4;  // >= 4 pad words after the indices: the dedup loop's read-ahead stays inside the row
     while ((rw & 7) != 4) rw += 4;
     g.row_words = rw;
     g.rk_stride = bs + 4;  // odd number of words: same-slot byte stores of a warp are conflict-free
@@ -338,11 +338,10 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
     const uint32_t a_tab0 = sbase + row_bytes * T;                         // table
     const uint32_t a_idtab = a_tab0 + 4u * t;                              // + 4*T*slot
     const uint32_t a_ranks0 = a_tab0 + 4u * T * S;                         // rank rows
-    const uint32_t a_ranks = a_ranks0 + (uint32_t)g.rk_stride * t;
+    uint32_t a_ranks = a_ranks0 + (uint32_t)g.rk_stride * t;
     const uint32_t a_rounds0 = a_ranks0 + (uint32_t)g.rk_stride * T;       // round records [round][thread]
     const uint32_t a_rounds = a_rounds0 + 4u * t;
     const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&s_bar);
-
     // static batching (batching.py:76-84): batch b = [first + b * bs, min(.. + bs, last_end)); the
     // caller's claim is verified off the critical path below
     const int first = __ldg(c.bbegin), last_end = __ldg(c.bend + (c.n_batches - 1));
@@ -372,6 +371,11 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         }
     };
     zero_table();
+    // the rows start as zeros: whatever the dedup loop reads past a row's last index (its read-ahead, a
+    // finished lane's current slot) is then a valid id: zero, a stale index or claim of an earlier tile
+    for (uint32_t o = 16u * t; o < row_bytes * T; o += 16u * NT)
+        asm volatile("st.shared.v4.u32 [%0], {%1,%1,%1,%1};" ::"r"(sbase + o), "r"(0u) : "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // ordered before the bulk copies into the rows
     // launched as a programmatic dependent of init_kernel: everything above overlapped its tail
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (t == 0) {
@@ -429,7 +433,11 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         // not claim, so the only branches are the loop and the (rare) round end.
         constexpr uint32_t kTagInc = 1u << LOG2W;
         constexpr uint32_t kTagMask = 0xFFu & ~(uint32_t)(W - 1);
-        const uint32_t a_dummy = a_rounds + 4u * T * (uint32_t)g.max_rounds;  // one spare word per thread
+        uint32_t a_dummy = a_rounds + 4u * T * (uint32_t)g.max_rounds;  // one spare word per thread
+        // opaque from here on: otherwise the compiler recomputes both from the shared-memory base inside
+        // the loop (~10 instructions per four trips) to save two registers
+        a_dummy = __shfl_sync(0xffffffffu, a_dummy, lane);  // (ptxas rematerialises anything it can see through)
+        a_ranks = __shfl_sync(0xffffffffu, a_ranks, lane);
         int p = 0, fill = 0, cursor = 0, rounds = 0;
         uint32_t cl = a_row;  // next claim slot of the row
         uint32_t tagw = kTagInc;
@@ -438,7 +446,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         // every index is range-checked as it becomes the lane's current slot: the packed table entry
         // holds 24 bits (vertex_count <= 2^24 on this path) and the gather must stay inside the buffer
         const uint32_t vcount = (uint32_t)sp.vertex_count;
-        bool bad = n > 0 && x >= vcount;
+        uint32_t mx = x;  // largest id seen; slots past the row's end hold valid ids (see the zeroing above)
         uint32_t h = (x * 0x9E3779B1u) >> (32 - LOG2S);
         uint32_t ai = a_idtab + 4u * T * h;  // address of the probed table slot
         uint32_t v = lds_u32(ai), cand = lds_u32(ax + 4);
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                 // that cannot be assigned (free slot reached), or the W-wide fetch in which the last
                 // claim was made is exhausted: fetches start at cursor, cursor + W, ... and a new one
                 // starts only while a lane is free (strategies.py:201, :220).
-                const bool ends = live & (fill == W) & (fre | (((p - cursor) & (W - 1)) == 0));
+                const bool ends = (fill == W) & (fre | (((p - cursor) & (W - 1)) == 0));
                 const bool adv = live & (hit | fre) & !ends;
                 const bool clm = adv & fre;  // strategies.py:207-212: new id -> lowest free lane
                 sts_u32(clm ? ai : a_dummy, xk | (uint32_t)fill);  // before the next probe is loaded
@@ -467,11 +475,11 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                 // claim list and local index: written unconditionally, a lane that does not resolve slot
                 // p here overwrites both when it does (the addresses only move on adv / clm)
                 sts_u32(cl, x);
-                sts_u8(a_ranks + (uint32_t)p, hit ? tq : (uint32_t)fill);
+                sts_u8(a_ranks + (uint32_t)p, min(tq, (uint32_t)fill));  // hit: tq = rank < fill; new claim: tq >= W >= fill
                 cl += clm ? 4u : 0u;
                 fill += clm ? 1 : 0;
                 p += adv ? 1 : 0;
-                bad |= (p < n) & (xn >= vcount);
+                mx = max(mx, xn);
                 ax = axn; x = xn; h = hn; ai = ain;
                 if (ends) {
                     const int d = p - cursor;
@@ -499,7 +507,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
             if (!__any_sync(0xffffffffu, p < n)) break;
         }
             VR_MARK(3);
-            if (active && bad) {
+            if (active && mx >= vcount) {
                 report_error(c, b, VR_ERR_BAD_BATCH);  // index outside the vertex buffer
                 active = false;
             }
@@ -507,7 +515,10 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                 report_error(c, b, VR_ERR_BAD_BATCH);  // not the static batching this path was promised
                 active = false;
             }
-            if (active) {  // the batch end closes the last round; nothing is discarded
+            // the batch end closes the last round; nothing is discarded.  (`ends` does not look at `live`: a
+            // finished lane with all W lanes claimed may already have recorded exactly this round, from
+            // whatever id follows the row: then cursor == n.)
+            if (active && cursor < n) {
                 sts_u32(a_rounds + 4u * T * rounds, ((uint32_t)((n - cursor) / 3) << 8) | (uint32_t)fill);
                 rounds++;
             }
