@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VRGEOM_ABI_VERSION 1
+#define VRGEOM_ABI_VERSION 2
 
 /* strategies.py:387  STRATEGY_NAMES = ("naive", "warp", "sort", "hash", "phash") */
 enum vr_strategy {
@@ -108,6 +108,11 @@ typedef struct vr_shader {
     const uint32_t *d_attributes; /* optional opaque per-vertex payload (mesh.py:40-41), or NULL */
     int32_t attr_words;        /* 32-bit words of payload per vertex                         */
     int32_t vertex_count;      /* 0 if unknown; needed for d_shade_counts                    */
+    const int32_t *d_batch_vertex_base; /* multi-draw: ids of batch b are relative to vertex
+                                  d_batch_vertex_base[b] of the (concatenated) vertex buffers: the
+                                  shader reads positions/attributes at base + id and tallies
+                                  d_shade_counts[base + id]; unique ids stay draw-local, as the
+                                  reference's per-draw runs report them.  NULL = one vertex buffer */
 } vr_shader;
 
 /* Statistics block: int64[VR_STATS_WORDS] in device memory, written by vr_run.
@@ -164,6 +169,21 @@ size_t vr_dynamic_workspace_bytes(int64_t n_indices, const vr_batch_config *cfg)
 int vr_dynamic_batches(const uint32_t *d_indices, int64_t n_indices, const vr_batch_config *cfg,
                        int32_t *d_offsets, int64_t *d_n_batches, void *d_workspace,
                        size_t workspace_bytes, void *stream);
+
+/* Multi-draw streams (BASELINE.json configs[4]; the reference calls dynamic_batches and
+ * run_on_indices once per mesh, strategies.py:404-415): the index buffers of n_draws draws are
+ * concatenated, draw d owning positions [d_draw_index_start[d], d_draw_index_start[d+1]) with
+ * [0] = 0 and [n_draws] = n_indices (device int32[n_draws+1], primitive-aligned, verified on the
+ * device).  Every draw restarts the greedy scan, so no batch crosses a draw; the offsets are
+ * positions in the concatenated buffer.  NULL / 0 draws = vr_dynamic_batches. */
+int vr_dynamic_batches_draws(const uint32_t *d_indices, int64_t n_indices, const vr_batch_config *cfg,
+                             const int32_t *d_draw_index_start, int32_t n_draws, int32_t *d_offsets,
+                             int64_t *d_n_batches, void *d_workspace, size_t workspace_bytes,
+                             void *stream);
+/* Per-batch first vertex for vr_shader.d_batch_vertex_base: batch b lies in the draw that holds
+ * d_batch_begin[b]; d_out[b] = d_draw_vertex_base[that draw] (device int32 arrays). */
+int vr_batch_vertex_base(const int32_t *d_batch_begin, int64_t n_batches, const int32_t *d_draw_index_start,
+                         const int32_t *d_draw_vertex_base, int32_t n_draws, int32_t *d_out, void *stream);
 
 /* Upper bounds for the data-dependent output sizes of vr_run. */
 int vr_output_bounds(int strategy, int64_t span_total, int64_t n_batches, const vr_batch_config *cfg,

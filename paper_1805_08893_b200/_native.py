@@ -45,7 +45,7 @@ class HashConfigC(C.Structure):
 class ShaderC(C.Structure):
     _fields_ = [("kind", C.c_int32), ("has_matrix", C.c_int32), ("matrix", C.c_float * 16),
                 ("d_positions4", C.c_void_p), ("d_attributes", C.c_void_p), ("attr_words", C.c_int32),
-                ("vertex_count", C.c_int32)]
+                ("vertex_count", C.c_int32), ("d_batch_vertex_base", C.c_void_p)]
 
 
 class OutputsC(C.Structure):
@@ -69,6 +69,10 @@ _SIGNATURES = {
     "vr_dynamic_workspace_bytes": (C.c_size_t, [C.c_int64, C.POINTER(BatchConfigC)]),
     "vr_dynamic_batches": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(BatchConfigC), C.c_void_p,
                                      C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_dynamic_batches_draws": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(BatchConfigC), C.c_void_p, C.c_int32,
+                                           C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_batch_vertex_base": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                       C.c_void_p]),
     "vr_output_bounds": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.POINTER(BatchConfigC),
                                    C.POINTER(HashConfigC), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "vr_run_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int64, C.c_int64, C.POINTER(BatchConfigC),
@@ -104,7 +108,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.vr_abi_version() != 1:
+        if handle.vr_abi_version() != 2:
             raise NativeLibraryError("libvrgeom.so ABI version mismatch")
         _lib = handle
     return _lib

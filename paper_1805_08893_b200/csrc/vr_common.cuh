@@ -83,6 +83,7 @@ struct ShaderParams {
     const uint32_t* __restrict__ attr;
     int attr_words;
     int vertex_count;
+    const int32_t* __restrict__ batch_base;  // multi-draw: first vertex of each batch's draw, or NULL
 };
 
 // The w-divide uses one hardware reciprocal (MUFU.RCP, <= 1 ulp) and three multiplies: a few ulp

@@ -53,6 +53,10 @@ struct DynCtx {
     int32_t* c_base;   // [n_chunks]
     int32_t* offsets;  // out
     int64_t* n_batches;  // out: [0] count, [1] status
+    // multi-draw streams: draw d owns positions [draw_start[d], draw_start[d+1]); a batch never
+    // crosses a draw (the reference runs dynamic_batches once per draw).  NULL = one draw.
+    const int32_t* __restrict__ draw_start;
+    int n_draws;
 };
 
 __global__ void fill_kernel(int32_t* p, int n, int v) {
@@ -127,9 +131,23 @@ __global__ void __launch_bounds__(128) greedy_next_kernel(DynCtx c, int run) {
     const int s1 = min(c.T, s0 + run);
     const int ps = c.ps;
     int e = s0, cnt = 0;
+    // multi-draw: the window never grows past the end of the draw that holds its first primitive.
+    // Occurrence links that cross a draw boundary are harmless: a link to an earlier draw lies
+    // before every window start of this draw, a link to a later one past every window end.
+    int d = 0, dend = c.T;
+    if (c.draw_start) {
+        int lo = 0, hi = c.n_draws;  // last d with draw_start[d] <= ps * s0
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (c.draw_start[mid] <= ps * s0) lo = mid; else hi = mid;
+        }
+        d = lo;
+        dend = c.draw_start[d + 1] / ps;
+    }
     for (int s = s0; s < s1; s++) {
         const int S = ps * s;
-        const int lim = min(c.T, s + c.cap);
+        while (s >= dend) dend = c.draw_start[++d + 1] / ps;  // (only with draws: dend == T otherwise)
+        const int lim = min(dend, s + c.cap);
         if (e < s) { e = s; cnt = 0; }
         while (e < lim) {
             int fresh = 0;
@@ -144,6 +162,18 @@ __global__ void __launch_bounds__(128) greedy_next_kernel(DynCtx c, int run) {
         for (int k = 0; k < ps; k++) lost += c.nxt[S + k] >= E;
         cnt -= lost;
     }
+}
+
+// draw table sanity (multi-draw): starts at 0, ends at n, non-decreasing, primitive-aligned
+__global__ void draws_check_kernel(DynCtx c) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d > c.n_draws) return;
+    const int v = c.draw_start[d];
+    bool bad = v % c.ps != 0 || v < 0 || v > c.n;
+    if (d == 0) bad |= v != 0;
+    if (d == c.n_draws) bad |= v != c.n;
+    if (d < c.n_draws) bad |= c.draw_start[d + 1] < v;
+    if (bad) c.n_batches[1] = VR_ERR_BAD_BATCH;
 }
 
 // ---- B1: chunk tables ---------------------------------------------------------------------
@@ -274,6 +304,13 @@ size_t vr_dynamic_workspace_bytes(int64_t n, const vr_batch_config* cfg) {
 
 int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg, int32_t* d_offsets,
                        int64_t* d_n_batches, void* d_ws, size_t ws_bytes, void* stream_) {
+    return vr_dynamic_batches_draws(d_idx, n, cfg, nullptr, 0, d_offsets, d_n_batches, d_ws, ws_bytes, stream_);
+}
+
+int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg,
+                             const int32_t* d_draw_index_start, int32_t n_draws, int32_t* d_offsets,
+                             int64_t* d_n_batches, void* d_ws, size_t ws_bytes, void* stream_) {
+    if (d_draw_index_start && n_draws <= 0) return VR_ERR_BAD_BATCH;
     int st = vr_check_batch_config(cfg);
     if (st) return st;
     if (n % cfg->primitive_size != 0) return VR_ERR_UNALIGNED;  // batching.py:96-97
@@ -305,6 +342,7 @@ int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* 
     c.g_entry = (int32_t*)(ws + L.g_entry); c.g_base = (int32_t*)(ws + L.g_base);
     c.c_entry = (int32_t*)(ws + L.c_entry); c.c_base = (int32_t*)(ws + L.c_base);
     c.offsets = d_offsets; c.n_batches = d_n_batches;
+    c.draw_start = d_draw_index_start; c.n_draws = d_draw_index_start ? n_draws : 0;
 
     fill_kernel<<<(int)ceil_div(n, 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
     const int n_tiles = (int)ceil_div(n, L.tile);
@@ -321,6 +359,7 @@ int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* 
     chunk_table_kernel<<<L.n_chunks, 256, 0, stream>>>(c);
     group_table_kernel<<<L.n_groups, 256, 0, stream>>>(c);
     group_scan_kernel<<<1, 32, 0, stream>>>(c);
+    if (c.draw_start) draws_check_kernel<<<(n_draws + 256) / 256, 256, 0, stream>>>(c);
     chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
     emit_offsets_kernel<<<(int)ceil_div(L.n_chunks, 128), 128, 0, stream>>>(c);
     VR_CUDA_CHECK(cudaGetLastError());

@@ -1259,7 +1259,7 @@ constexpr int kShadeUnroll = 4;
 // (l = lane within the group): coalesced id load, 16-byte gather, transform, coalesced stores.
 template <int STRATEGY>
 __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams& sp, const uint32_t* __restrict__ src,
-                                             int cnt, int64_t dst0, int l, int width, int naive_mo) {
+                                             int cnt, int64_t dst0, int l, int width, int naive_mo, int vbase) {
     const bool want_uid = c.out.d_unique_ids != nullptr;
     const bool want_pos = sp.kind == VR_SHADER_POSITION;
     const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
@@ -1278,7 +1278,7 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
 #pragma unroll
             for (int u = 0; u < kShadeUnroll; u++) {
                 const int j = j0 + u * width + l;
-                if (j < cnt) p[u] = __ldg(sp.pos4 + uid[u]);
+                if (j < cnt) p[u] = __ldg(sp.pos4 + vbase + uid[u]);
             }
         }
 #pragma unroll
@@ -1290,8 +1290,8 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
             if (STRATEGY == VR_NAIVE && c.out.d_assembly_map) c.out.d_assembly_map[naive_mo + j] = (uint16_t)(j % c.ps);
             if (want_attr)
                 for (int k = 0; k < sp.attr_words; k++)
-                    c.out.d_shaded_attr[(dst0 + j) * sp.attr_words + k] = __ldg(sp.attr + (int64_t)uid[u] * sp.attr_words + k);
-            if (want_cnt) atomicAdd(&c.out.d_shade_counts[uid[u]], 1);
+                    c.out.d_shaded_attr[(dst0 + j) * sp.attr_words + k] = __ldg(sp.attr + ((int64_t)vbase + uid[u]) * sp.attr_words + k);
+            if (want_cnt) atomicAdd(&c.out.d_shade_counts[vbase + uid[u]], 1);
         }
     }
 }
@@ -1328,6 +1328,7 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
         // comes from one warp-wide OR: lane L sets the bit of the last output of its batch, and an
         // output's owner is the first owner of the step plus the number of batch ends before it.
         const unsigned long long my_src = (unsigned long long)(c.stage_uid + stage_uid_base(c, b, mo));
+        const int my_vbase = valid && sp.batch_base ? __ldg(sp.batch_base + b) : 0;
         const int ex = inc_u - cnt.y;
         const int tot = __shfl_sync(0xffffffffu, inc_u, 31);
         const bool want_uid = c.out.d_unique_ids != nullptr;
@@ -1340,6 +1341,7 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
         int first_owner = 0;
         for (int j0 = 0; j0 < tot; j0 += 32 * kShadeUnroll) {
             uint32_t uid[kShadeUnroll];
+            int vb[kShadeUnroll];
             float4 p[kShadeUnroll];
 #pragma unroll
             for (int u = 0; u < kShadeUnroll; u++) {
@@ -1350,13 +1352,14 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
                 first_owner += __popc(ends);
                 const int oex = __shfl_sync(0xffffffffu, ex, owner);
                 const uint32_t* osrc = (const uint32_t*)__shfl_sync(0xffffffffu, my_src, owner);
+                vb[u] = __shfl_sync(0xffffffffu, my_vbase, owner);
                 const int j = jb + lane;
                 uid[u] = j < tot ? osrc[j - oex] : 0u;
             }
             if (want_pos) {
 #pragma unroll
                 for (int u = 0; u < kShadeUnroll; u++)
-                    if (j0 + 32 * u + lane < tot) p[u] = __ldg(sp.pos4 + uid[u]);
+                    if (j0 + 32 * u + lane < tot) p[u] = __ldg(sp.pos4 + vb[u] + uid[u]);
             }
 #pragma unroll
             for (int u = 0; u < kShadeUnroll; u++) {
@@ -1366,8 +1369,8 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
                 if (want_pos) shaded[j] = transform_position(sp, p[u]);
                 if (want_attr)
                     for (int k = 0; k < sp.attr_words; k++)
-                        c.out.d_shaded_attr[((int64_t)off.y + j) * sp.attr_words + k] = __ldg(sp.attr + (int64_t)uid[u] * sp.attr_words + k);
-                if (want_cnt) atomicAdd(&c.out.d_shade_counts[uid[u]], 1);
+                        c.out.d_shaded_attr[((int64_t)off.y + j) * sp.attr_words + k] = __ldg(sp.attr + ((int64_t)vb[u] + uid[u]) * sp.attr_words + k);
+                if (want_cnt) atomicAdd(&c.out.d_shade_counts[vb[u] + uid[u]], 1);
             }
         }
     } else {
@@ -1390,7 +1393,7 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
             }
             src = c.stage_uid + stage_uid_base(c, b, mo);
         }
-        shade_stream<STRATEGY>(c, sp, src, cnt.y, off.y, lane, 32, mo);
+        shade_stream<STRATEGY>(c, sp, src, cnt.y, off.y, lane, 32, mo, sp.batch_base ? __ldg(sp.batch_base + b) : 0);
     }
 }
 
@@ -1443,6 +1446,22 @@ __global__ void __launch_bounds__(1024) span_only_scan_kernel(const int32_t* __r
         __syncthreads();
     }
     if (tid == 0) map_off[n_batches] = (int32_t)carry;
+}
+
+// multi-draw: first vertex of the draw that holds each batch (include/vrgeom.h vr_batch_vertex_base)
+__global__ void __launch_bounds__(256) batch_vertex_base_kernel(const int32_t* __restrict__ bbegin, int64_t nb,
+                                                                const int32_t* __restrict__ draw_start,
+                                                                const int32_t* __restrict__ draw_vbase, int n_draws,
+                                                                int32_t* __restrict__ out) {
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const int pos = bbegin[b];
+    int lo = 0, hi = n_draws;  // last draw with draw_start[d] <= pos (empty draws share a start: the last one wins)
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (draw_start[mid] <= pos) lo = mid; else hi = mid;
+    }
+    out[b] = draw_vbase[lo];
 }
 
 __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __restrict__ off) {
@@ -1712,6 +1731,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         for (int i = 0; i < 16; i++) sp.m[i] = shader->matrix[i];
         sp.pos4 = (const float4*)shader->d_positions4; sp.attr = shader->d_attributes;
         sp.attr_words = shader->d_attributes ? shader->attr_words : 0; sp.vertex_count = shader->vertex_count;
+        sp.batch_base = shader->d_batch_vertex_base;
         if (sp.kind == VR_SHADER_POSITION && (!sp.pos4 || !out->d_shaded4)) return VR_ERR_BAD_CONFIG;
     }
     const int nbi = (int)nb;
@@ -1733,7 +1753,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         VR_CUDA_CHECK(cudaFuncSetAttribute(hash_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
 
-    const bool fast_warp = strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0 && nb > 0;
+    // (the position-aligned kernels read one vertex buffer: multi-draw runs take the general path)
+    const bool fast_warp = strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0 && nb > 0 && !sp.batch_base;
     const bool fused = fast_warp && allow_fuse;
     // tile kernel (vr_warp_rows.cuh) when a batch row fits shared memory comfortably
     RowsGeom rg{};
@@ -1840,6 +1861,18 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
 
 int vr_last_launch_count(void) { return g_last_launches; }
 int vr_last_kernel_path(void) { return g_last_path; }
+
+int vr_batch_vertex_base(const int32_t* d_batch_begin, int64_t n_batches, const int32_t* d_draw_index_start,
+                         const int32_t* d_draw_vertex_base, int32_t n_draws, int32_t* d_out, void* stream) {
+    if (n_batches < 0 || n_draws <= 0 || !d_draw_index_start || !d_draw_vertex_base) return VR_ERR_BAD_BATCH;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (n_batches == 0) return VR_OK;
+    if (!d_batch_begin || !d_out) return VR_ERR_BAD_BATCH;
+    batch_vertex_base_kernel<<<(int)ceil_div(n_batches, 256), 256, 0, (cudaStream_t)stream>>>(
+        d_batch_begin, n_batches, d_draw_index_start, d_draw_vertex_base, n_draws, d_out);
+    VR_CUDA_CHECK(cudaGetLastError());
+    return VR_OK;
+}
 
 #ifdef VR_TIMELINE
 // debugging aid (not part of the ABI): copies the phase time stamps of the last tile-kernel launch

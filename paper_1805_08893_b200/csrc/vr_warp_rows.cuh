@@ -447,13 +447,21 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         // holds 24 bits (vertex_count <= 2^24 on this path) and the gather must stay inside the buffer
         const uint32_t vcount = (uint32_t)sp.vertex_count;
         uint32_t mx = x;  // largest id seen; slots past the row's end hold valid ids (see the zeroing above)
-        uint32_t h = (x * 0x9E3779B1u) >> (32 - LOG2S);
-        uint32_t ai = a_idtab + 4u * T * h;  // address of the probed table slot
+        uint32_t ai = a_idtab + 4u * T * ((x * 0x9E3779B1u) >> (32 - LOG2S));  // address of the probed table slot
+        const uint32_t a_tab_end = a_idtab + 4u * T * S;
         uint32_t v = lds_u32(ai), cand = lds_u32(ax + 4);
         for (;;) {
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const bool live = p < n;
+                // off the critical path (known before the probe v arrives): the slot a collision moves
+                // to, the slot the next id hashes to, and the part of the round-end test that does not
+                // depend on the probe
+                uint32_t a_coll = ai + 4u * T;
+                a_coll -= a_coll >= a_tab_end ? 4u * T * S : 0u;
+                const uint32_t a_cand = a_idtab + 4u * T * ((cand * 0x9E3779B1u) >> (32 - LOG2S));
+                const bool full = fill == W;
+                const bool full_edge = full & (((p - cursor) & (W - 1)) == 0);
                 const uint32_t xk = x * 256u + tagw;              // id << 8 | tag: one IMAD
                 const uint32_t tq = v ^ xk;                       // == rank (< W) iff the slot holds x in this round
                 const bool hit = tq < (uint32_t)W;
@@ -462,14 +470,12 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                 // that cannot be assigned (free slot reached), or the W-wide fetch in which the last
                 // claim was made is exhausted: fetches start at cursor, cursor + W, ... and a new one
                 // starts only while a lane is free (strategies.py:201, :220).
-                const bool ends = (fill == W) & (fre | (((p - cursor) & (W - 1)) == 0));
+                const bool ends = full_edge | (full & fre);
                 const bool adv = live & (hit | fre) & !ends;
                 const bool clm = adv & fre;  // strategies.py:207-212: new id -> lowest free lane
                 sts_u32(clm ? ai : a_dummy, xk | (uint32_t)fill);  // before the next probe is loaded
                 const uint32_t xn = adv ? cand : x;
-                const uint32_t hx = (xn * 0x9E3779B1u) >> (32 - LOG2S);
-                const uint32_t hn = (hit | fre) ? hx : ((h + 1) & (S - 1));
-                const uint32_t ain = a_idtab + 4u * T * hn;
+                const uint32_t ain = adv ? a_cand : a_coll;  // (a resolved probe that does not advance is a round end or a finished lane)
                 const uint32_t axn = ax + (adv ? 4u : 0u);
                 uint32_t vn = lds_u32(ain), candn = lds_u32(axn + 4);
                 // claim list and local index: written unconditionally, a lane that does not resolve slot
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                 fill += clm ? 1 : 0;
                 p += adv ? 1 : 0;
                 mx = max(mx, xn);
-                ax = axn; x = xn; h = hn; ai = ain;
+                ax = axn; x = xn; ai = ain;
                 if (ends) {
                     const int d = p - cursor;
                     const int emitted = (int)(((uint32_t)d * 43691u) >> 17);  // d / 3 for d < 2^16
@@ -491,8 +497,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
                     p = cursor;  // re-open at the first unconsumed slot (the row still holds it: see slack)
                     ax = a_ids + 4u * (uint32_t)p;
                     x = lds_u32(ax);
-                    h = (x * 0x9E3779B1u) >> (32 - LOG2S);
-                    ai = a_idtab + 4u * T * h;
+                    ai = a_idtab + 4u * T * ((x * 0x9E3779B1u) >> (32 - LOG2S));
                     if (tagw == kTagMask) {  // tag space exhausted: wipe this thread's column
 #pragma unroll 1
                         for (int k = 0; k < S; k++) sts_u32(a_idtab + 4u * T * k, 0u);

@@ -142,6 +142,7 @@ class ShaderSpec:
     matrix: np.ndarray | None = None
     attributes: torch.Tensor | None = None  # int32[V, words]
     vertex_count: int = 0
+    batch_vertex_base: torch.Tensor | None = None  # int32[n_batches]: multi-draw (draws.py)
 
 
 class DeviceRun:
@@ -291,6 +292,8 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
     sh = N.ShaderC()
     sh.kind = shader.kind
     sh.vertex_count = shader.vertex_count
+    if shader.batch_vertex_base is not None:
+        sh.d_batch_vertex_base = shader.batch_vertex_base.data_ptr()
     if shader.kind == N.VR_SHADER_POSITION:
         run.shaded4 = g("shaded", max_inv.value * 4, torch.float32, dev).view(-1, 4)
         sh.d_positions4 = shader.positions4.data_ptr()

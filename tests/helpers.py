@@ -53,3 +53,52 @@ def next_pow2(x):
     while p < x:
         p *= 2
     return p
+
+
+def oracle_draws(O, strategy, meshes, *, dynamic=True, batch_size=96, max_unique=256, max_indices=1023,
+                 warp_width=32, table_size=256, max_fast_probes=8, matrix=None, shade=True):
+    """The reference's way through a multi-draw scene: dynamic_batches / static_batches and
+    run_on_indices once per mesh (strategies.py:404-415), concatenated in draw order."""
+    offs, bro, ruo, rp, uid, amap, shaded, counts = [], [0], [0], [], [], [], [], []
+    tot = dict(rounds=0, invocations=0, indices=0, probes_fast=0, probes_slow=0, probe_max_chain=0)
+    per_draw = []
+    ipos = 0
+    for m in meshes:
+        idx = np.asarray(m.indices, dtype=np.uint32)
+        if dynamic:
+            so = O.dynamic_batches(idx, max_unique=max_unique, max_indices=max_indices)
+        else:
+            so = O.static_batches(len(idx), batch_size=batch_size)
+        if len(so) == 0:
+            per_draw.append((0, 0))
+            counts.append(np.zeros(m.vertex_count, dtype=np.int64))
+            continue
+        fr = O.run(strategy, idx, so[:-1], so[1:], max_unique=max_unique, warp_width=warp_width,
+                   table_size=table_size, max_fast_probes=max_fast_probes)
+        offs.append(so[:-1] + ipos)
+        bro.extend((fr.batch_round_off[1:] + bro[-1]).tolist())
+        ruo.extend((fr.round_uid_off[1:] + ruo[-1]).tolist())
+        rp.append(fr.round_prims)
+        uid.append(fr.unique_ids)
+        amap.append(fr.assembly_map)
+        if shade:
+            shaded.append(O.shade_positions(m.positions, fr.unique_ids, matrix))
+        counts.append(O.shade_counts(fr.unique_ids, m.vertex_count))
+        for k in ("rounds", "invocations", "indices", "probes_fast", "probes_slow"):
+            tot[k] += getattr(fr, k)
+        tot["probe_max_chain"] = max(tot["probe_max_chain"], fr.probe_max_chain)  # ProbeStats.merge
+        per_draw.append((len(so) - 1, fr.invocations))
+        ipos += len(idx)
+    cat = lambda parts, dt: np.concatenate(parts).astype(dt) if parts else np.zeros(0, dtype=dt)
+    total_idx = sum(len(m.indices) for m in meshes)
+    flat = {
+        "batch_round_off": np.asarray(bro, dtype=np.int64),
+        "round_uid_off": np.asarray(ruo, dtype=np.int64),
+        "round_prims": cat(rp, np.int32),
+        "unique_ids": cat(uid, np.uint32),
+        "assembly_map": cat(amap, np.int32),
+    }
+    offsets = np.concatenate([cat(offs, np.int64), [total_idx]]) if offs else np.zeros(0, dtype=np.int64)
+    return dict(flat=flat, offsets=offsets, totals=tot, per_draw=per_draw,
+                shaded=np.concatenate(shaded) if shaded else np.zeros((0, 3), np.float32),
+                counts=cat(counts, np.int64))
