@@ -53,6 +53,13 @@ WORKLOADS = {
 }
 
 
+# configs[4]: oracle totals of the 1000-draw scene (scripts/c5_expect.py; dynamic 256/1023 per draw)
+C5_EXPECT = {
+    "sort": dict(batches=154797, rounds=154797, invocations=39026006),
+    "hash": dict(batches=154797, rounds=154797, invocations=39026006, probes_fast=328902576),
+}
+
+
 def algorithmic_bytes(n_idx, n_inv, n_batches):
     """SURVEY.md 8(d) / BASELINE.md section 3: uint32 index read + float4 position read and float4
     shaded write per invocation + uint16 local-index write + 12 B of batch metadata."""
@@ -395,6 +402,59 @@ def main():
                        "statistics block read back; shaded vertices/triangles stay on the GPU for the next stage"}
         return res, e2e
 
+    def run_multidraw(strategy, steps, warmup):
+        """BASELINE.json configs[4]: 1000 draws, 20.4 M triangles, dynamic 256/1023 batches per
+        draw, packed into one stream (paper_1805_08893_b200/draws.py).  Two figures: dedup + shade with the
+        offsets precomputed (as the paper reports dynamic batching), and including batch formation."""
+        from paper_1805_08893_b200 import draws as D
+        cfg = __import__("paper_1805_08893_b200").BatchConfig()
+        hcfg = HashConfig(table_size=cfg.block_size)
+        ds = D.pack_draws(D.scene_corpus(1000), dev)
+        tris = ds.triangles
+        bufs = engine.RunBuffers()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        ws = torch.empty(lib.vr_dynamic_workspace_bytes(ds.indices.numel(), C.byref(engine._cfg_c(cfg))),
+                         dtype=torch.uint8, device=dev)
+        offs = D.dynamic_offsets_draws(ds, cfg, ws)
+        vbase = D.batch_vertex_base(ds, offs)
+        nb = offs.numel() - 1
+        exp = C5_EXPECT[strategy]
+        for _ in range(max(warmup, 1)):
+            run = D.run_draws(strategy, ds, offs, cfg, hcfg, matrix=MATRIX, buffers=bufs, vbase=vbase)
+        run.check()
+        got = dict(batches=nb, rounds=run.rounds, invocations=run.invocations)
+        if strategy == "hash":
+            got["probes_fast"] = run.probes[0]
+        assert got == exp, f"parity gate failed: {got} != {exp}"
+
+        def timed(fn):
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            torch.cuda.synchronize()
+            for k in range(steps):
+                flush.zero_()
+                evs[k][0].record()
+                fn()
+                evs[k][1].record()
+            torch.cuda.synchronize()
+            return float(np.mean([a.elapsed_time(b) for a, b in evs]))
+
+        ms_run = timed(lambda: D.run_draws(strategy, ds, offs, cfg, hcfg, matrix=MATRIX, buffers=bufs, vbase=vbase))
+
+        def whole():
+            o = D.dynamic_offsets_draws(ds, cfg, ws)  # (reads the batch count back: one host round trip)
+            vb = D.batch_vertex_base(ds, o, vbase)
+            D.run_draws(strategy, ds, o, cfg, hcfg, matrix=MATRIX, buffers=bufs, vbase=vb)
+        whole()
+        ms_whole = timed(whole)
+        inv = run.invocations
+        alg = algorithmic_bytes(ds.indices.numel(), inv, nb)
+        return {"value": tris / (ms_run * 1e-3), "ms_per_step": ms_run,
+                "value_incl_batch_formation": tris / (ms_whole * 1e-3), "ms_incl_batch_formation": ms_whole,
+                "draws": ds.n_draws, "triangles": tris, "vertices": int(ds.vertex_base[-1]), "batches": nb,
+                "invocations": inv, "reuse_rate": 1 - inv / ds.indices.numel(),
+                "stage_roofline": {"algorithmic_bytes": alg, "frac": alg / (ms_run * 1e-3) / 1e9 / 6557.1},
+                "gpu_launches": steps * lib.vr_last_launch_count()}
+
     import ctypes as C
     res, e2e = run_workload(args.workload, args.steps, args.warmup, True)
     others = {}
@@ -403,6 +463,8 @@ def main():
             if name != args.workload:
                 r, _ = run_workload(name, max(10, args.steps // 5), args.warmup, False)
                 others[name] = r
+        for strat in ("sort", "hash"):
+            others[f"c5_multidraw_{strat}"] = run_multidraw(strat, max(10, args.steps // 5), args.warmup)
     wl = WORKLOADS[args.workload]
     line = {
         "metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,

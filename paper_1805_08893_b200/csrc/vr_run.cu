@@ -51,6 +51,7 @@ struct RunCtx {
     long long* acc;         // [ACC_WORDS]
     unsigned long long* tile_state;  // [n_fused_tiles] decoupled look-back: flag<<62 | rounds<<32 | ids
     int n_fused_tiles;
+    int n_state_words;  // words of tile_state to clear: the tiles, and for the tile kernel its group tables behind them
     // outputs
     vr_outputs out;
 };
@@ -91,7 +92,7 @@ __global__ void init_kernel(RunCtx c) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the tile kernel may be scheduled; it waits below
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < ACC_WORDS) c.acc[i] = 0;
-    if (i < c.n_fused_tiles) c.tile_state[i] = 0ull;
+    if (i < c.n_state_words) c.tile_state[i] = 0ull;
 }
 
 // Non-contiguous batch lists: single-CTA scan of the spans (general path, not the hot one).
@@ -1497,7 +1498,8 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.tile_sums = o; o += align_up((size_t)(L.n_scan_tiles + 1) * 8);
     L.tile_off = o; o += align_up((size_t)(L.n_scan_tiles + 2) * 8);
     L.acc = o; o += align_up(ACC_WORDS * 8);
-    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 64) + 1) * 8);  // kRowThreads tiles (>= kFastThreads tiles)
+    // kRowThreads tiles (>= kFastThreads tiles) + the tile kernel's two group tables (one group = 32 tiles)
+    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 64) + 1 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);
     L.stage_uid = o;
     if (strategy != VR_NAIVE) {
         size_t words = (size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64;
@@ -1766,7 +1768,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     g_prof_marks = 0;
     g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : 0;
     prof_mark(stream);
-    init_kernel<<<(int)ceil_div(c.n_fused_tiles + ACC_WORDS, 256), 256, 0, stream>>>(c);
+    c.n_state_words = rows ? c.n_fused_tiles + 1 + 2 * ((int)ceil_div(c.n_fused_tiles, kRowGroup) + 1) : c.n_fused_tiles;
+    init_kernel<<<(int)ceil_div(c.n_state_words + ACC_WORDS, 256), 256, 0, stream>>>(c);
     if (!contiguous && nb > 0) span_scan_kernel<<<1, 1024, 0, stream>>>(c);
     prof_mark(stream);
     if (nb > 0) {

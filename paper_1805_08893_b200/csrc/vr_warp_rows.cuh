@@ -32,6 +32,7 @@
 // Debug / tuning knobs (environment, read at launch): VR_LAG=<K>, VR_PREFETCH=1, VR_NO_PDL=1.
 #pragma once
 
+constexpr int kRowGroup = 32;    // tiles per group of the two-level offset scan
 constexpr int kRowThreads = 64;      // batches per tile = dedup threads
 constexpr int kRowCtaThreads = 192;  // + 4 helper warps
 
@@ -44,6 +45,7 @@ struct RowsGeom {
     int tile_words;  // scratch words per tile: meta[2][64] | rounds[64][max_rounds] | claims[64 * row_cap]
     int lag;         // K: the helpers of the CTA with ticket i shade tile i - K
     int n_tiles;
+    int n_groups;  // groups of kRowGroup tiles (two-level offset scan)
     uint32_t cpr_magic;  // ceil(2^32 / (batch_size / 8)): chunk -> row by multiply-high
     size_t smem;
 };
@@ -188,54 +190,80 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
         for (int u = 0; u < U8; u++)  // the next step's vertices: on their way to L2 while this step is shaded
             if (ht + NH * (U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
     }
-    // ---- D: output offsets of tile stile by decoupled look-back (first helper warp)
+    // ---- D: output offsets of tile stile (first helper warp).  All ~600 tiles in flight reach this
+    // point together, so a tile-by-tile look-back would have to walk ~600 aggregates (five dependent
+    // round trips to L2).  Two levels instead: every tile adds its aggregate to its GROUP's sum when
+    // it publishes; a tile's exclusive prefix is (inclusive prefix of the previous group, found by a
+    // decoupled look-back over groups: 64 groups = 2048 tiles per step) + (aggregates of the earlier
+    // tiles of its own group).  All loads of both levels are in flight together: one round trip.
     if (lb_warp) {
         const long long ar = (long long)((mine >> 32) & 0x3FFFFFFFull), au = (long long)(mine & 0xFFFFFFFFull);
-        // Each step inspects the 128 nearest predecessors (4 per lane, all loads in flight
-        // together); the walk ends at the nearest tile that already holds an inclusive prefix.
+        unsigned long long* __restrict__ grp_sum = c.tile_state + g.n_tiles + 1;   // count<<58 | rounds<<34 | claims
+        unsigned long long* __restrict__ grp_incl = grp_sum + g.n_groups + 1;      // flag<<62 | rounds<<32 | claims
+        const int grp = stile / kRowGroup, pos = stile % kRowGroup;
         long long pr = 0, pu = 0;  // this lane's share of the exclusive prefix of the tile
-        bool found = false;
-        constexpr int LB = 4;
-        for (int pz = stile - 1; pz >= 0 && !found && !lost; pz -= 32 * LB) {
-            unsigned long long word[LB];
+        bool found = grp == 0;
+        constexpr int LB = 2;
+        bool first = true;
+        for (int pz = grp - 1; (first || (pz >= 0 && !found)) && !lost; pz -= 32 * LB) {
+            unsigned long long word[LB], sum[LB], tw = 0;
             int spins = 0;
             for (;;) {
                 bool pending = false;
+                if (first && lane < pos) tw = ld_relaxed_gpu_u64(c.tile_state + grp * kRowGroup + lane);
 #pragma unroll
                 for (int k = 0; k < LB; k++) {
                     const int idx = pz - lane - 32 * k;
-                    word[k] = ld_relaxed_gpu_u64(c.tile_state + (idx >= 0 ? idx : 0));
+                    word[k] = found ? 0ull : ld_relaxed_gpu_u64(grp_incl + (idx >= 0 ? idx : 0));
+                    sum[k] = found ? 0ull : ld_relaxed_gpu_u64(grp_sum + (idx >= 0 ? idx : 0));
                 }
+                if (first && lane < pos) pending |= (tw >> 62) == 0;
 #pragma unroll
                 for (int k = 0; k < LB; k++) {
-                    if (pz - lane - 32 * k < 0) word[k] = kStateInclusive + 0ull;  // before the first tile: inclusive zero
-                    pending |= (word[k] >> 62) == 0;
+                    if (pz - lane - 32 * k < 0) word[k] = kStateInclusive + 0ull;  // before the first group: inclusive zero
+                    // (every group before the last one holds kRowGroup tiles)
+                    pending |= !found && (word[k] >> 62) == 0 && (sum[k] >> 58) != (unsigned long long)kRowGroup;
                 }
                 if (!__any_sync(0xffffffffu, pending)) break;
                 if (++spins > (1 << 22)) { lost = true; break; }
             }
             if (lost) break;
+            if (first && lane < pos) {
+                pr += (long long)((tw >> 32) & 0x3FFFFFFFull);
+                pu += (long long)(tw & 0xFFFFFFFFull);
+            }
 #pragma unroll
             for (int k = 0; k < LB; k++) {
-                const uint32_t incl = __ballot_sync(0xffffffffu, (word[k] >> 62) == 2);
+                const uint32_t incl = __ballot_sync(0xffffffffu, !found && (word[k] >> 62) == 2);
                 const int upto = found ? -1 : (incl ? __ffs(incl) - 1 : 31);
-                if (lane <= upto) {
+                if (lane < upto) {  // nearer groups: their complete sums
+                    pr += (long long)((sum[k] >> 34) & 0xFFFFFFull);
+                    pu += (long long)(sum[k] & 0x3FFFFFFFFull);
+                } else if (lane == upto && incl) {  // the nearest group that knows its inclusive prefix
                     pr += (long long)((word[k] >> 32) & 0x3FFFFFFFull);
                     pu += (long long)(word[k] & 0xFFFFFFFFull);
+                } else if (lane == upto) {
+                    pr += (long long)((sum[k] >> 34) & 0xFFFFFFull);
+                    pu += (long long)(sum[k] & 0x3FFFFFFFFull);
                 }
                 found |= incl != 0;
             }
+            first = false;
         }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             pr += __shfl_xor_sync(0xffffffffu, pr, d);
             pu += __shfl_xor_sync(0xffffffffu, pu, d);
         }
+        if (lane == 0 && !lost) {
+            // the last tile of a group knows the group's inclusive prefix: later groups stop there
+            if (pos == kRowGroup - 1)
+                st_relaxed_gpu_u64(grp_incl + grp, kStateInclusive | ((unsigned long long)((pr + ar) & 0x3FFFFFFF) << 32) | (unsigned long long)((pu + au) & 0xFFFFFFFFll));
+        }
         const long long er = pr, eu = pu;
         if (lane == 0) {
             if (lost) report_error(c, (int64_t)stile * T, VR_ERR_CUDA);
             const long long R = er + ar, U = eu + au;
-            st_relaxed_gpu_u64(c.tile_state + stile, kStateInclusive | ((unsigned long long)(R & 0x3FFFFFFF) << 32) | (unsigned long long)(U & 0xFFFFFFFFll));
             const bool fits = U <= c.out.cap_unique && R <= c.out.cap_rounds && U <= 0x7fffffffLL && !lost;
             if (!fits) report_error(c, (int64_t)stile * T, VR_ERR_CAPACITY);
             s_base = fits ? make_int2((int)er, (int)eu) : make_int2(-1, -1);
@@ -645,6 +673,10 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         if (t == 0 && has_tile) {
             __threadfence();
             st_relaxed_gpu_u64(c.tile_state + tile, aggregate);
+            // ... and into the tile's group: count << 58 | rounds << 34 | claims (the value is the message:
+            // a reader that sees count == kRowGroup has the complete sum)
+            atomicAdd(c.tile_state + g.n_tiles + 1 + tile / kRowGroup,
+                      (1ull << 58) | (((aggregate >> 32) & 0x3FFFFFFFull) << 34) | (aggregate & 0xFFFFFFFFull));
         }
         VR_MARK(5);
         tile = next;
@@ -668,6 +700,7 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRowCtaThreads, g.smem);
     g.n_tiles = (int)ceil_div(c.n_batches, kRowThreads);
+    g.n_groups = (int)ceil_div(g.n_tiles, kRowGroup);
     const char* e = getenv("VR_LAG");
     const int resident = sms * (per_sm > 0 ? per_sm : 1);
     // Tickets go round the persistent CTAs, so tile i - resident is the CTA's own previous tile and its

@@ -57,3 +57,6 @@ stat("  wait aggregate", h[8, sel] - h[7, sel])
 stat("  ids, gathers, look-back", h[9, sel] - h[8, sel])
 stat("  stores + further steps", h[10, sel] - h[9, sel])
 stat("  round tables", h[6, sel] - h[10, sel])
+hs = a[:, 1, :nt + lag]
+ends = hs[6][hs[6] > 0]
+print(f"last shading ends {(ends.max() - t0) / 1e3:.1f} us after the first ticket; tail after the last publish {(ends.max() - d[5].max()) / 1e3:.1f} us")

@@ -120,3 +120,36 @@ def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
         assert_flat_equal(sub.flat(), oracle_flat(fr), f"config4 {strat} prefix")
         if strat in ("hash", "phash"):
             assert sub.probes == (fr.probes_fast, fr.probes_slow, fr.probe_max_chain)
+
+
+def test_config5_multidraw_scene(cuda_lib):
+    """BASELINE.json configs[4]: 1000 draws, 20 397 942 triangles, 10 319 577 vertices, dynamic 256/1023
+    batches per draw, sort and hash dedup.  Everything is compared with the per-mesh oracle runs:
+    boundaries, every round, every local index, statistics, per-vertex tallies."""
+    from helpers import oracle_draws
+    from paper_1805_08893_b200 import draws as D
+    meshes = D.scene_corpus(1000)
+    ds = D.pack_draws(meshes)
+    assert (ds.triangles, int(ds.vertex_base[-1])) == (20_397_942, 10_319_577)
+    cfg = BatchConfig()
+    offsets = D.dynamic_offsets_draws(ds, cfg)
+    for strategy in ("sort", "hash"):
+        want = oracle_draws(O, strategy, meshes, matrix=MATRIX, shade=False)
+        assert np.array_equal(offsets.cpu().numpy().astype(np.int64), want["offsets"])
+        run = D.run_draws(strategy, ds, offsets, cfg, HashConfig(), matrix=MATRIX, want_counts=True)
+        flat = run.flat()
+        assert_flat_equal(flat, want["flat"], f"c5 {strategy}")
+        t = want["totals"]
+        assert (len(offsets) - 1, run.invocations, run.rounds) == (154_797, 39_026_006, 154_797)
+        assert (run.invocations, run.rounds, run.indices) == (t["invocations"], t["rounds"], t["indices"])
+        if strategy == "hash":
+            assert run.probes == (t["probes_fast"], 0, t["probe_max_chain"]) and run.probes[0] == 328_902_576
+        assert np.array_equal(flat["shade_counts"], want["counts"])
+        # shaded positions: spot-check three draws against the float64 shader
+        for d in (0, 501, 999):
+            b0 = int(np.searchsorted(want["offsets"][:-1], ds.index_start[d]))
+            b1 = int(np.searchsorted(want["offsets"][:-1], ds.index_start[d + 1]))
+            ruo, bro = want["flat"]["round_uid_off"], want["flat"]["batch_round_off"]
+            u0, u1 = int(ruo[bro[b0]]), int(ruo[bro[b1]])
+            ref = O.shade_positions(meshes[d].positions, want["flat"]["unique_ids"][u0:u1], MATRIX)
+            np.testing.assert_allclose(flat["shaded"][u0:u1, :3], ref, rtol=1e-5, atol=1e-5)
