@@ -161,6 +161,19 @@ class DeviceRun:
         self.kernel_path = 0
         self._stats = None
 
+    def relaunch(self) -> "DeviceRun":
+        """Issue vr_run with the prepared arguments on the current stream (see run_device)."""
+        lib = N.require_cuda()
+        if self.shade_counts is not None:
+            self.shade_counts.zero_()
+        with torch.cuda.device(self._device):
+            st = lib.vr_run(*self._args, _stream_ptr())
+        raise_status(st)
+        self._stats = None
+        self.launches = lib.vr_last_launch_count()  # kernels this call launched (bench.py's gpu_launches)
+        self.kernel_path = lib.vr_last_kernel_path()  # 3 = persistent tile kernel (include/vrgeom.h)
+        return self
+
     # -- statistics -----------------------------------------------------------------
     def stats(self) -> np.ndarray:
         if self._stats is None:
@@ -257,8 +270,12 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                n_batches: int, span_total: int, max_span: int, cfg: BatchConfig, hcfg=None,
                shader: ShaderSpec | None = None, *, want_counts: bool = False,
                buffers: RunBuffers | None = None, enforce_budget: bool = True,
-               contiguous: bool | None = None, static: bool = False, fuse: bool = True) -> DeviceRun:
-    """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back."""
+               contiguous: bool | None = None, static: bool = False, fuse: bool = True,
+               plan_only: bool = False) -> DeviceRun:
+    """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back.
+    `plan_only` prepares buffers and arguments without launching: `.relaunch()` then issues the same
+    run again (same inputs, outputs overwritten) at the cost of one C call, for callers that repeat a
+    run of one shape (a frame loop, bench.py)."""
     lib = N.require_cuda()
     if strategy not in N.STRATEGY_IDS:
         raise ConfigError(f"unknown strategy {strategy!r}; expected one of {tuple(N.STRATEGY_IDS)}")
@@ -316,12 +333,10 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         run.shaded_attr.data_ptr() if run.shaded_attr is not None else None,
         run.shade_counts.data_ptr() if run.shade_counts is not None else None,
         run.stats_dev.data_ptr(), max_inv.value, max_rounds.value)
-    with torch.cuda.device(dev):
-        st = lib.vr_run(sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
-                        span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws),
-                        ws.numel(), _stream_ptr())
-    raise_status(st)
-    run.launches = lib.vr_last_launch_count()  # kernels this call launched (bench.py's gpu_launches)
-    run.kernel_path = lib.vr_last_kernel_path()  # 3 = persistent tile kernel (include/vrgeom.h)
-    run._keep = (ws, shader)
-    return run
+    args = (sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
+            span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws), ws.numel())
+    run._keep = (ws, shader, c, h, sh, out, d_indices, d_begin, d_end)
+    run._args, run._device = args, dev
+    if plan_only:
+        return run
+    return run.relaunch()
