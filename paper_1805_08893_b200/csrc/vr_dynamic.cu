@@ -123,6 +123,97 @@ __global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_t
     }
 }
 
+// ---- A1, tile version ------------------------------------------------------------------------
+// One CTA per tile of positions (+ a halo of one batch window), one THREAD per position, no
+// warp-synchronous probing: the positions are bucketed by id with a counting sort over the slots of
+// a shared open-addressing table (insert + count, scan, scatter), then every tile position takes the
+// largest earlier position in its bucket.  Buckets are unordered (the scatter uses atomics), so a
+// position reads its whole bucket: a few entries for any mesh-like stream; ids with very many
+// occurrences inside the window fall back to walking the index buffer backwards (their previous
+// occurrence is then near on average).  Used when tile + halo fit 16-bit relative positions.
+constexpr int kLinkThreads = 256;
+constexpr int kBigBucket = 48;
+
+__global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(DynCtx c, int tile, int halo, int nslots) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);          // [nslots]
+    uint32_t* cnt = keys + nslots;                                    // [nslots + 1] count, then bucket end
+    uint16_t* slot_of = reinterpret_cast<uint16_t*>(cnt + nslots + 1);  // [tile + halo]
+    uint16_t* bucket = slot_of + tile + halo;                         // [tile + halo] relative positions
+    __shared__ uint32_t s_part[kLinkThreads];
+    const int t = threadIdx.x;
+    const int t0 = blockIdx.x * tile;
+    const int t1 = min(c.n, t0 + tile);
+    int hs = t0 - halo;
+    if (hs < 0) hs = 0;
+    const int np = t1 - hs;  // positions of halo + tile
+    for (int i = t; i <= nslots; i += kLinkThreads) {
+        if (i < nslots) keys[i] = kEmpty;
+        cnt[i] = 0;
+    }
+    __syncthreads();
+    // insert + count
+    for (int r = t; r < np; r += kLinkThreads) {
+        const uint32_t id = c.ids[hs + r];
+        uint32_t h = __umulhi(id * 0x9E3779B1u, (uint32_t)nslots);
+        for (;;) {
+            const uint32_t k = atomicCAS(&keys[h], kEmpty, id);
+            if (k == kEmpty || k == id) break;
+            h = h + 1 == (uint32_t)nslots ? 0u : h + 1;
+        }
+        slot_of[r] = (uint16_t)h;
+        atomicAdd(&cnt[h], 1u);
+    }
+    __syncthreads();
+    // exclusive scan of the counts -> bucket starts (cnt[h] becomes the start; the scatter turns it into the end)
+    {
+        const int per = (nslots + kLinkThreads - 1) / kLinkThreads;
+        const int lo = t * per, hi = min(nslots, lo + per);
+        uint32_t sum = 0;
+        for (int i = lo; i < hi; i++) sum += cnt[i];
+        s_part[t] = sum;
+        __syncthreads();
+        if (t < 32) {  // 256 partials: 8 per lane
+            uint32_t v[8], tot = 0;
+            for (int k = 0; k < 8; k++) { v[k] = s_part[t * 8 + k]; tot += v[k]; }
+            uint32_t inc = tot;
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (t >= d) inc += o;
+            }
+            uint32_t run = inc - tot;
+            for (int k = 0; k < 8; k++) { s_part[t * 8 + k] = run; run += v[k]; }
+        }
+        __syncthreads();
+        uint32_t run = s_part[t];
+        for (int i = lo; i < hi; i++) { const uint32_t v = cnt[i]; cnt[i] = run; run += v; }
+    }
+    __syncthreads();
+    // scatter
+    for (int r = t; r < np; r += kLinkThreads) bucket[atomicAdd(&cnt[slot_of[r]], 1u)] = (uint16_t)r;
+    __syncthreads();
+    // nearest earlier occurrence of every tile position
+    for (int r = t0 - hs + t; r < np; r += kLinkThreads) {
+        const uint32_t h = slot_of[r];
+        const uint32_t end = cnt[h], begin = h ? cnt[h - 1] : 0u;  // starts are the previous slot's end
+        int pv = -1;
+        if (end - begin <= (uint32_t)kBigBucket) {
+            for (uint32_t e = begin; e < end; e++) {
+                const int q = bucket[e];
+                if (q < r && q > pv) pv = q;
+            }
+        } else {
+            const uint32_t id = c.ids[hs + r];
+            for (int q = r - 1; q >= 0; q--)
+                if (c.ids[hs + q] == id) { pv = q; break; }
+        }
+        const int i = hs + r;
+        const int pva = pv >= 0 ? hs + pv : -1;
+        c.prev[i] = pva;
+        if (pva >= 0) c.nxt[pva] = i;
+    }
+}
+
 // ---- A2 -----------------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) greedy_next_kernel(DynCtx c, int run) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -346,7 +437,16 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
 
     fill_kernel<<<(int)ceil_div(n, 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
     const int n_tiles = (int)ceil_div(n, L.tile);
-    if (small_last) {
+    // tile version: thread per position, counting sort by table slot (16-bit relative positions)
+    const int halo2 = (L.window + 31) & ~31;
+    const int tile2 = 4096;
+    const int np2 = tile2 + halo2;
+    const int nslots2 = ((np2 + np2 / 4) + 31) & ~31;
+    const size_t smem2 = (size_t)nslots2 * 4 + (size_t)(nslots2 + 1) * 4 + (size_t)np2 * 4 + 16;
+    if (np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !getenv("VR_LINKS_WARP")) {
+        VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+        occurrence_links_tile_kernel<<<(int)ceil_div(n, tile2), kLinkThreads, smem2, stream>>>(c, tile2, halo2, nslots2);
+    } else if (small_last) {
         VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         occurrence_links_kernel<uint16_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
     } else {

@@ -306,3 +306,32 @@ def test_determinism_across_launches(cuda_lib):
         f = run.flat()
         blobs.append(b"".join(np.ascontiguousarray(f[k]).tobytes() for k in FLAT_KEYS) + bytes(str(run.probes), "ascii"))
     assert blobs[0] == blobs[1] == blobs[2]
+
+
+def test_dynamic_adversarial_streams(cuda_lib):
+    """Batch formation against the oracle on streams that stress the occurrence links: one id, a
+    handful of ids (buckets far beyond the in-bucket scan limit), long runs, a pool around the
+    budget, long windows (both link kernels), primitive size 1."""
+    rng = np.random.default_rng(99)
+    n = 3 * 40_000
+    runs = np.repeat(rng.integers(0, 1 << 20, size=n // 50 + 1), 50)[:n]
+    streams = {
+        "one-id": np.full(n, 5, dtype=np.uint32),
+        "two-ids": (np.arange(n) % 2).astype(np.uint32),
+        "five-ids": rng.integers(0, 5, size=n).astype(np.uint32),
+        "pool-300": rng.integers(0, 300, size=n).astype(np.uint32),
+        "pool-60": rng.integers(0, 60, size=n).astype(np.uint32),
+        "runs": runs.astype(np.uint32),
+        "all-new": np.arange(n, dtype=np.uint32),
+        "far-repeat": np.concatenate([np.arange(2000), np.arange(2000)] * 30).astype(np.uint32)[:n],
+    }
+    cfgs = [dict(), dict(max_unique=8), dict(max_unique=3, max_indices=30), dict(max_unique=256, max_indices=4095),
+            dict(max_unique=1000, max_indices=8191), dict(max_unique=16, max_indices=64, primitive_size=1),
+            dict(max_unique=50, max_indices=1023)]
+    for name, ids in streams.items():
+        for kw in cfgs:
+            ps = kw.get("primitive_size", 3)
+            cfg = BatchConfig(batch_size=96 if ps == 3 else 32, **kw)
+            want = O.dynamic_batches(ids, primitive_size=ps, max_unique=cfg.max_unique, max_indices=cfg.max_indices)
+            got = engine.dynamic_offsets_device(ids, cfg).cpu().numpy().astype(np.int64)
+            assert np.array_equal(got, want), f"{name} {kw}: first difference at batch {int(np.argmax(got[:len(want)] != want[:len(got)]))}"
