@@ -768,6 +768,108 @@ __global__ void __launch_bounds__(256) sort_batch_kernel(RunCtx c, int pmax) {
 }
 
 // ---------------------------------------------------------------------------------
+// K1 (sort), one WARP per batch: the result of strategies.py:235-260 is "unique ids ascending,
+// local index = rank of the id", which does not need the batch sorted -- only its DISTINCT ids
+// (at most max_unique of them under the budget of strategies.py:451-455).  So: (1) distinct ids
+// by insertion into a private open-addressing set (CAS), remembering every element's set slot;
+// (2) the distinct ids are compacted out of the set and sorted (bitonic, in shared memory, padded
+// to the next power of two of their number); (3) every sorted id looks its set slot up again and
+// leaves its rank there; (4) local index of element i = rank at its set slot.
+// ---------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int q, int u_bound, int p_max, int per_warp_bytes) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int warps = blockDim.x >> 5;
+    const int b = blockIdx.x * warps + wid;
+    if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
+    unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
+    uint32_t* ids = reinterpret_cast<uint32_t*>(base);
+    uint32_t* kkey = ids + n_max;                                      // [q] the set
+    uint32_t* sorted = kkey + q;                                       // [p_max]
+    uint16_t* kslot = reinterpret_cast<uint16_t*>(sorted + p_max);     // [n_max] set slot of every element
+    uint16_t* rank_at = kslot + n_max;                                 // [q] rank of the id in a set slot
+    int begin, n;
+    if (!validate_batch(c, b, begin, n)) {
+        if (lane == 0) c.counts[b] = make_int2(0, 0);
+        return;
+    }
+    const int mo = batch_map_off(c, b, begin);
+    const uint32_t qmask = (uint32_t)q - 1;
+    const int qbits = ilog2((uint32_t)q);
+    for (int i = lane; i < n; i += 32) ids[i] = __ldg(c.idx + begin + i);
+    for (int i = lane; i < q; i += 32) kkey[i] = kEmpty;
+    __syncwarp();
+    int fresh = 0;
+    bool overflow = false;
+    for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        if (i < n) {
+            const uint32_t id = ids[i];
+            uint32_t h = (id * 0x9E3779B1u) >> (32 - qbits);
+            for (;;) {
+                const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
+                if (prev == kEmpty) fresh++;
+                if (prev == kEmpty || prev == id) break;
+                h = (h + 1) & qmask;
+            }
+            kslot[i] = (uint16_t)h;
+        }
+        int tot = fresh;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+        if (tot > u_bound) { overflow = true; break; }  // uniform: stop before the set can fill up
+    }
+    if (overflow) {  // only under the unique budget: more distinct ids than max_unique (strategies.py:451-455)
+        if (lane == 0) {
+            report_error(c, b, VR_ERR_OVER_BUDGET);
+            c.counts[b] = make_int2(0, 0);
+        }
+        return;
+    }
+    __syncwarp();
+    // distinct ids out of the set
+    int nu = 0;
+    for (int s0 = 0; s0 < q; s0 += 32) {
+        const uint32_t k = kkey[s0 + lane];
+        const uint32_t m = __ballot_sync(0xffffffffu, k != kEmpty);
+        if (k != kEmpty) sorted[nu + __popc(m & ((1u << lane) - 1))] = k;
+        nu += __popc(m);
+    }
+    const int P = (int)next_pow2((uint32_t)max(nu, 2));
+    for (int i = nu + lane; i < P; i += 32) sorted[i] = kEmpty;  // pads sort last
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = lane; t < (P >> 1); t += 32) {
+                const int lo = 2 * t - (t & (j - 1));
+                const int hi = lo + j;
+                const bool asc = (lo & k) == 0;
+                const uint32_t a = sorted[lo], d = sorted[hi];
+                if ((a > d) == asc) { sorted[lo] = d; sorted[hi] = a; }
+            }
+            __syncwarp();
+        }
+    }
+    uint32_t* __restrict__ suid = c.stage_uid + stage_uid_base(c, b, mo);
+    for (int r = lane; r < nu; r += 32) {
+        const uint32_t id = sorted[r];
+        uint32_t h = (id * 0x9E3779B1u) >> (32 - qbits);
+        while (kkey[h] != id) h = (h + 1) & qmask;
+        rank_at[h] = (uint16_t)r;
+        suid[r] = id;
+    }
+    __syncwarp();
+    if (c.out.d_assembly_map) {
+        uint16_t* __restrict__ amap = c.out.d_assembly_map + mo;
+        for (int i = lane; i < n; i += 32) amap[i] = rank_at[kslot[i]];
+    }
+    if (lane == 0) {
+        c.counts[b] = make_int2(1, nu);
+        if (c.enforce_budget && nu > c.max_unique) report_error(c, b, VR_ERR_OVER_BUDGET);
+    }
+}
+
+// ---------------------------------------------------------------------------------
 // K1 (hash): strategies.py:263-298 -- Algorithm 3, bit-exact with the reference's
 // sequential insertion order for any thread schedule:
 //   phase 1  first occurrence of every id (set insert into a private table with CAS,
@@ -1814,7 +1916,21 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             VR_CUDA_CHECK(cudaFuncSetAttribute(phash_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
             phash_warp_kernel<<<(int)ceil_div(nb, warps), warps * 32, wsmem, stream>>>(c, wn, cfg->warp_width, (int)hc.max_fast_probes, per_warp);
         } else if (strategy == VR_SORT) {
-            sort_batch_kernel<<<nbi, 256, smem, stream>>>(c, pmax);
+            // one warp per batch (distinct ids, then a sort of those only) when its tables fit; else the CTA sort
+            const int u_bound = c.enforce_budget && cfg->max_unique < max_span ? cfg->max_unique : max_span;
+            const int wn = (max_span + 31) & ~31;
+            const int wq = (int)next_pow2((uint32_t)(2 * (u_bound + 32)));
+            const int wp = (int)next_pow2((uint32_t)(u_bound + 32));
+            const int per_warp = (wn * 4 + wq * 4 + wp * 4 + wn * 2 + wq * 2 + 15) & ~15;
+            if (per_warp <= 24 * 1024 && wq <= 65536 && !getenv("VR_SORT_CTA")) {
+                int warps = 8;
+                while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
+                const size_t wsmem = (size_t)warps * per_warp;
+                VR_CUDA_CHECK(cudaFuncSetAttribute(sort_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsmem));
+                sort_warp_kernel<<<(int)ceil_div(nb, warps), warps * 32, wsmem, stream>>>(c, wn, wq, u_bound, wp, per_warp);
+            } else {
+                sort_batch_kernel<<<nbi, 256, smem, stream>>>(c, pmax);
+            }
         } else {
             // one warp per batch when a warp's tables fit comfortably; else one CTA per batch
             const int u_bound = (uint32_t)max_span < hc.table_size ? max_span : (int)hc.table_size;
