@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_t
 }
 
 // ---- A1, tile version ------------------------------------------------------------------------
-// One CTA per tile of positions (+ a halo of one batch window), one THREAD per position, no
+// One CTA per tile of 2048 positions (+ a halo of one batch window), one THREAD per position, no
 // warp-synchronous probing: the positions are bucketed by id with a counting sort over the slots of
 // a shared open-addressing table (insert + count, scan, scatter), then every tile position takes the
 // largest earlier position in its bucket.  Buckets are unordered (the scatter uses atomics), so a
@@ -439,7 +439,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     const int n_tiles = (int)ceil_div(n, L.tile);
     // tile version: thread per position, counting sort by table slot (16-bit relative positions)
     const int halo2 = (L.window + 31) & ~31;
-    const int tile2 = 4096;
+    const int tile2 = getenv("VR_LINK_TILE") ? atoi(getenv("VR_LINK_TILE")) : 2048;  // (4096 / 6144: fewer CTAs per SM, measured slower)
     const int np2 = tile2 + halo2;
     const int nslots2 = ((np2 + np2 / 4) + 31) & ~31;
     const size_t smem2 = (size_t)nslots2 * 4 + (size_t)(nslots2 + 1) * 4 + (size_t)np2 * 4 + 16;
@@ -453,7 +453,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
         VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         occurrence_links_kernel<int32_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
     }
-    const int run = 64;
+    const int run = getenv("VR_GREEDY_RUN") ? atoi(getenv("VR_GREEDY_RUN")) : 64;
     const int n_threads = (int)ceil_div(L.T, run);
     greedy_next_kernel<<<(int)ceil_div(n_threads, 128), 128, 0, stream>>>(c, run);
     chunk_table_kernel<<<L.n_chunks, 256, 0, stream>>>(c);

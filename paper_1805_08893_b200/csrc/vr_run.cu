@@ -1922,7 +1922,10 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             const int wq = (int)next_pow2((uint32_t)(2 * (u_bound + 32)));
             const int wp = (int)next_pow2((uint32_t)(u_bound + 32));
             const int per_warp = (wn * 4 + wq * 4 + wp * 4 + wn * 2 + wq * 2 + 15) & ~15;
-            if (per_warp <= 24 * 1024 && wq <= 65536 && !getenv("VR_SORT_CTA")) {
+            // (a few long batches -- configs[0]: 509 batches of 768 -- do not fill the GPU with one warp each:
+            // the CTA sort is faster there)
+            const bool few_long = nb < 2048 && wp > 512;
+            if (per_warp <= 24 * 1024 && wq <= 65536 && !few_long && !getenv("VR_SORT_CTA")) {
                 int warps = 8;
                 while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
                 const size_t wsmem = (size_t)warps * per_warp;

@@ -153,3 +153,20 @@ def test_config5_multidraw_scene(cuda_lib):
             u0, u1 = int(ruo[bro[b0]]), int(ruo[bro[b1]])
             ref = O.shade_positions(meshes[d].positions, want["flat"]["unique_ids"][u0:u1], MATRIX)
             np.testing.assert_allclose(flat["shaded"][u0:u1, :3], ref, rtol=1e-5, atol=1e-5)
+
+
+def test_sort_long_static_batches_both_kernels(cuda_lib):
+    """configs[0]'s batch shape (static 768, up to 768 distinct ids) on a mesh with enough batches
+    that the warp-per-batch sort kernel is chosen (>= 2048), and on a prefix that takes the CTA sort."""
+    mesh = P.gen_grid(560, 560)
+    cfg = BatchConfig(batch_size=768, max_unique=768, block_size=1024)
+    for n_idx in (len(mesh.indices), 768 * 300):
+        idx = mesh.indices[:n_idx]
+        so = O.static_batches(n_idx, batch_size=768)
+        assert (len(so) - 1 >= 2048) == (n_idx == len(mesh.indices))
+        fr = O.run("sort", idx, so[:-1], so[1:], max_unique=768)
+        d_idx = engine.to_device_indices(idx)
+        offs = engine.static_offsets_device(n_idx, cfg)
+        run = engine.run_device("sort", d_idx, offs[:-1], offs[1:], offs.numel() - 1, n_idx, 768, cfg, None,
+                                engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
+        assert_flat_equal(run.flat(), oracle_flat(fr), f"static-768 sort, {len(so) - 1} batches")
