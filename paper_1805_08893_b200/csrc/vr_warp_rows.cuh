@@ -20,8 +20,9 @@
 //                (8 x uint16); then the tile's (rounds, claims) AGGREGATE is published.  The CTA
 //                never waits for the tile's output offsets.
 //   helper warps, tile j = i - K  (K = 1.5 x the number of CTAs: tile j was published half a round ago)
-//     D  offsets decoupled look-back over the published aggregates (no waiting in the steady
-//                state); publishes j's inclusive prefix;
+//     D  offsets two-level scan: j's exclusive prefix = inclusive prefix of the previous 32-tile GROUP
+//                (decoupled look-back over group sums that the tiles accumulate when they publish)
+//                + the aggregates of the earlier tiles of j's own group; one L2 round trip;
 //     E  shade   the tile's flat claim list is streamed from the scratch (L2 hits): coalesced id
 //                store, 16-byte position gather, FP32 4x4 transform + w-divide (strategies.py:53-67),
 //                coalesced 16-byte stores; round tables from the round records.

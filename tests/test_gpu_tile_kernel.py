@@ -1,5 +1,5 @@
 """The tile kernel of the static warp-voting path (csrc/vr_warp_rows.cuh): bulk-staged rows,
-per-lane state machine, decoupled shading K tiles later, drain kernel.  Everything is compared
+per-lane state machine, decoupled shading K tiles later, two-level offset scan, shade-only tail.  Everything is compared
 bit-exactly with the CPU oracle; the kernel is reached through vr_run with VR_FLAG_STATIC and a
 shader that states its vertex count (<= 2^24), exactly as bench.py does."""
 from __future__ import annotations
@@ -45,7 +45,7 @@ def blob(flat):
 
 def test_lag_does_not_change_results(cuda_lib):
     """The tile a CTA's helpers shade (ticket - K) is a scheduling choice: K = 1, a few, more than the
-    number of tiles (everything left to the drain kernel) and the default give identical bytes."""
+    number of tiles (everything left to the shade-only tickets) and the default give identical bytes."""
     mesh = P.gen_grid(300, 217)
     cfg = BatchConfig()
     spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
