@@ -44,6 +44,10 @@ def test_config3_warp(cuda_lib, dragon_grid, path):
     assert abs(1 - run.invocations / run.indices - 0.624846) < 1e-6
     assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
     assert int(run.shade_counts.sum().item()) == run.invocations
+    if path == "fused":  # the persistent tile kernel: every output of the full run against the C oracle
+        assert run.kernel_path == 3
+        so = O.static_batches(len(mesh.indices))
+        assert_flat_equal(run.flat(), oracle_flat(O.run("warp", mesh.indices, so[:-1], so[1:])), "config 3, tile kernel")
     # bit-exact against the oracle on a prefix and on a window in the middle of the stream
     for lo in (0, 3000 * 96 * 30):
         sub = mesh.indices[lo:lo + 96 * 3000 + 33]  # ragged last batch
