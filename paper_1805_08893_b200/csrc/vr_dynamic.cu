@@ -147,27 +147,40 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
     int hs = t0 - halo;
     if (hs < 0) hs = 0;
     const int np = t1 - hs;  // positions of halo + tile
+    const uint32_t mask = (uint32_t)nslots - 1, shift = (uint32_t)__clz(nslots) + 1;  // nslots is a power of two: 32 - log2
     for (int i = t; i <= nslots; i += kLinkThreads) {
         if (i < nslots) keys[i] = kEmpty;
         cnt[i] = 0;
     }
     __syncthreads();
-    // insert + count
-    for (int r = t; r < np; r += kLinkThreads) {
-        const uint32_t id = c.ids[hs + r];
-        uint32_t h = __umulhi(id * 0x9E3779B1u, (uint32_t)nslots);
-        for (;;) {
-            const uint32_t k = atomicCAS(&keys[h], kEmpty, id);
-            if (k == kEmpty || k == id) break;
-            h = h + 1 == (uint32_t)nslots ? 0u : h + 1;
+    // insert + count (the ids of four positions are loaded ahead of their insertions)
+    for (int r0 = t; r0 < np; r0 += 4 * kLinkThreads) {
+        uint32_t idv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) idv[u] = r0 + u * kLinkThreads < np ? c.ids[hs + r0 + u * kLinkThreads] : 0u;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            const int r = r0 + u * kLinkThreads;
+            if (r >= np) break;
+            const uint32_t id = idv[u];
+            // double hashing over a power-of-two table (odd step): at load 0.75 an insertion takes ~2 probes on
+            // average and the longest chain among the 32 lanes of a warp stays short; linear probing at the
+            // same load left most lanes idle behind the unluckiest one (ncu: 13 of 32 lanes active)
+            uint32_t h = (id * 0x9E3779B1u) >> shift;
+            const uint32_t step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
+            for (;;) {
+                const uint32_t k = atomicCAS(&keys[h], kEmpty, id);
+                if (k == kEmpty || k == id) break;
+                h = (h + step) & mask;
+            }
+            slot_of[r] = (uint16_t)h;
+            atomicAdd(&cnt[h], 1u);
         }
-        slot_of[r] = (uint16_t)h;
-        atomicAdd(&cnt[h], 1u);
     }
     __syncthreads();
     // exclusive scan of the counts -> bucket starts (cnt[h] becomes the start; the scatter turns it into the end)
     {
-        const int per = (nslots + kLinkThreads - 1) / kLinkThreads;
+        const int per = ((nslots + kLinkThreads - 1) / kLinkThreads) | 1;  // odd: the threads' chunks start on different banks
         const int lo = t * per, hi = min(nslots, lo + per);
         uint32_t sum = 0;
         for (int i = lo; i < hi; i++) sum += cnt[i];
@@ -251,6 +264,77 @@ __global__ void __launch_bounds__(128) greedy_next_kernel(DynCtx c, int run) {
         const int E = ps * e;
         int lost = 0;
         for (int k = 0; k < ps; k++) lost += c.nxt[S + k] >= E;
+        cnt -= lost;
+    }
+}
+
+// A2 with the links of a CTA's stretch of the stream staged in shared memory.  In the kernel above every
+// thread walks its own part of prev / nxt in global memory: a warp's 32 streams are 768 bytes apart, each
+// step waits for the slowest lane's cache miss, and a trip takes ~1 us (ncu: 12 % issue utilisation, 70 % of
+// the samples on the prev load).  Here the CTA first copies the links of its run of start primitives plus
+// one batch window, coalesced, as 16-bit DISTANCES (position - prev, next - position; 65535 = none, which
+// compares like "outside any window" because a window is shorter than that), then runs the same two-pointer
+// walk out of shared memory.
+__global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run, int npos_max) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint16_t* dp = reinterpret_cast<uint16_t*>(smem_raw);  // [npos_max] position - prev
+    uint16_t* dn = dp + npos_max;                          // [npos_max] next - position
+    const int ps = c.ps;
+    const int p0 = blockIdx.x * blockDim.x * run;          // first start primitive of the CTA
+    const int base = ps * p0;
+    const int npos = min(c.n - base, npos_max);
+    auto put = [&](int r, int pv, int nx) {
+        const int i = base + r;
+        dp[r] = (uint16_t)(pv < 0 ? 65535 : min(i - pv, 65535));
+        dn[r] = (uint16_t)(nx == kNoLink ? 65535 : min(nx - i, 65535));
+    };
+    if ((base & 3) == 0) {  // 16-byte loads, several in flight per thread: the copy is the bulk of this kernel's traffic
+        const int4* __restrict__ pv4 = reinterpret_cast<const int4*>(c.prev + base);
+        const int4* __restrict__ nx4 = reinterpret_cast<const int4*>(c.nxt + base);
+        const int nq = npos >> 2;
+#pragma unroll 4
+        for (int qd = threadIdx.x; qd < nq; qd += blockDim.x) {
+            const int4 a = __ldg(pv4 + qd), b = __ldg(nx4 + qd);
+            put(4 * qd, a.x, b.x); put(4 * qd + 1, a.y, b.y); put(4 * qd + 2, a.z, b.z); put(4 * qd + 3, a.w, b.w);
+        }
+        for (int r = 4 * nq + threadIdx.x; r < npos; r += blockDim.x) put(r, c.prev[base + r], c.nxt[base + r]);
+    } else {
+        for (int r = threadIdx.x; r < npos; r += blockDim.x) put(r, c.prev[base + r], c.nxt[base + r]);
+    }
+    __syncthreads();
+    const int s0 = p0 + threadIdx.x * run;
+    if (s0 >= c.T) return;
+    const int s1 = min(c.T, s0 + run);
+    int e = s0, cnt = 0;
+    int d = 0, dend = c.T;
+    if (c.draw_start) {
+        int lo = 0, hi = c.n_draws;  // last d with draw_start[d] <= ps * s0
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (c.draw_start[mid] <= ps * s0) lo = mid; else hi = mid;
+        }
+        d = lo;
+        dend = c.draw_start[d + 1] / ps;
+    }
+    for (int s = s0; s < s1; s++) {
+        const int S = ps * s;
+        while (s >= dend) dend = c.draw_start[++d + 1] / ps;
+        const int lim = min(dend, s + c.cap);
+        if (e < s) { e = s; cnt = 0; }
+        while (e < lim) {
+            int fresh = 0;
+            for (int k = 0; k < ps; k++) {
+                const int i = ps * e + k;
+                fresh += (int)dp[i - base] > i - S;  // prev < S
+            }
+            if (e != s && cnt + fresh > c.max_unique) break;  // first primitive always accepted
+            cnt += fresh;
+            e++;
+        }
+        c.next[s] = e;
+        const int E = ps * e;
+        int lost = 0;
+        for (int k = 0; k < ps; k++) lost += (int)dn[S + k - base] >= E - (S + k);  // next >= E
         cnt -= lost;
     }
 }
@@ -441,7 +525,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     const int halo2 = (L.window + 31) & ~31;
     const int tile2 = getenv("VR_LINK_TILE") ? atoi(getenv("VR_LINK_TILE")) : 2048;  // (4096 / 6144: fewer CTAs per SM, measured slower)
     const int np2 = tile2 + halo2;
-    const int nslots2 = ((np2 + np2 / 4) + 31) & ~31;
+    const int nslots2 = (int)next_pow2((uint32_t)(np2 + np2 / 3));  // load <= 0.75
     const size_t smem2 = (size_t)nslots2 * 4 + (size_t)(nslots2 + 1) * 4 + (size_t)np2 * 4 + 16;
     if (np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !getenv("VR_LINKS_WARP")) {
         VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
@@ -455,7 +539,18 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     }
     const int run = getenv("VR_GREEDY_RUN") ? atoi(getenv("VR_GREEDY_RUN")) : 64;
     const int n_threads = (int)ceil_div(L.T, run);
-    greedy_next_kernel<<<(int)ceil_div(n_threads, 128), 128, 0, stream>>>(c, run);
+    // shared-memory version when a CTA's stretch (128 runs + one batch window) fits as 16-bit distances
+    // (run * ps halfwords between the lanes' streams: an odd number of 32-bit words keeps their reads on
+    // different banks)
+    int run_s = 30;
+    while ((run_s * c.ps) % 4 != 2 && run_s < 33) run_s++;
+    const int64_t npos_s = (int64_t)128 * run_s * c.ps + L.window + c.ps;
+    if (npos_s * 4 <= 56 * 1024 && L.window < 60000 && !getenv("VR_GREEDY_GLOBAL")) {
+        VR_CUDA_CHECK(cudaFuncSetAttribute(greedy_next_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(npos_s * 4)));
+        greedy_next_smem_kernel<<<(int)ceil_div(L.T, 128 * run_s), 128, (size_t)npos_s * 4, stream>>>(c, run_s, (int)npos_s);
+    } else {
+        greedy_next_kernel<<<(int)ceil_div(n_threads, 128), 128, 0, stream>>>(c, run);
+    }
     chunk_table_kernel<<<L.n_chunks, 256, 0, stream>>>(c);
     group_table_kernel<<<L.n_groups, 256, 0, stream>>>(c);
     group_scan_kernel<<<1, 32, 0, stream>>>(c);
