@@ -59,9 +59,10 @@ struct DynCtx {
     int n_draws;
 };
 
+// (the buffer starts 256-byte aligned and is padded: whole 16-byte stores)
 __global__ void fill_kernel(int32_t* p, int n, int v) {
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = v;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (4 * i < n) reinterpret_cast<int4*>(p)[i] = make_int4(v, v, v, v);
 }
 
 // ---- A1 -----------------------------------------------------------------------------------
@@ -519,7 +520,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     c.offsets = d_offsets; c.n_batches = d_n_batches;
     c.draw_start = d_draw_index_start; c.n_draws = d_draw_index_start ? n_draws : 0;
 
-    fill_kernel<<<(int)ceil_div(n, 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
+    fill_kernel<<<(int)ceil_div(ceil_div(n, 4), 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
     const int n_tiles = (int)ceil_div(n, L.tile);
     // tile version: thread per position, counting sort by table slot (16-bit relative positions)
     const int halo2 = (L.window + 31) & ~31;

@@ -776,6 +776,49 @@ __global__ void __launch_bounds__(256) sort_batch_kernel(RunCtx c, int pmax) {
 // to the next power of two of their number); (3) every sorted id looks its set slot up again and
 // leaves its rank there; (4) local index of element i = rank at its set slot.
 // ---------------------------------------------------------------------------------
+// Bitonic sort of 32 * R keys held R per lane (key index = r * 32 + lane): partners at distance >= 32 are
+// registers of the same lane, nearer ones come by shuffle; no shared memory, no barriers.
+template <int R>
+__device__ __forceinline__ void warp_bitonic_regs(uint32_t (&v)[R], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    if ((r & jr) == 0) {
+                        const bool asc = ((r * 32) & k) == 0;  // k >= 64 here: the direction depends on r alone
+                        const uint32_t a = v[r], d = v[r | jr];
+                        const uint32_t lo = min(a, d), hi = max(a, d);
+                        v[r] = asc ? lo : hi;
+                        v[r | jr] = asc ? hi : lo;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    const uint32_t o = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool asc = (((r * 32) | lane) & k) == 0;
+                    const bool lower = (lane & j) == 0;
+                    v[r] = (lower == asc) ? min(v[r], o) : max(v[r], o);
+                }
+            }
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void warp_sort_shared(uint32_t* sorted, int lane) {
+    uint32_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) v[r] = sorted[r * 32 + lane];
+    warp_bitonic_regs<R>(v, lane);
+#pragma unroll
+    for (int r = 0; r < R; r++) sorted[r * 32 + lane] = v[r];
+}
+
 __global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int q, int u_bound, int p_max, int per_warp_bytes) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -835,10 +878,16 @@ __global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int
         if (k != kEmpty) sorted[nu + __popc(m & ((1u << lane) - 1))] = k;
         nu += __popc(m);
     }
-    const int P = (int)next_pow2((uint32_t)max(nu, 2));
+    const int P = (int)next_pow2((uint32_t)max(nu, 32));
     for (int i = nu + lane; i < P; i += 32) sorted[i] = kEmpty;  // pads sort last
     __syncwarp();
-    for (int k = 2; k <= P; k <<= 1) {
+    // up to 256 distinct ids (the default budget): sorted in registers; more: in shared memory
+    if (P == 32) warp_sort_shared<1>(sorted, lane);
+    else if (P == 64) warp_sort_shared<2>(sorted, lane);
+    else if (P == 128) warp_sort_shared<4>(sorted, lane);
+    else if (P == 256) warp_sort_shared<8>(sorted, lane);
+    __syncwarp();
+    for (int k = 2; k <= P && P > 256; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int t = lane; t < (P >> 1); t += 32) {
                 const int lo = 2 * t - (t & (j - 1));
