@@ -826,8 +826,7 @@ __global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int
     const int b = blockIdx.x * warps + wid;
     if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
     unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
-    uint32_t* ids = reinterpret_cast<uint32_t*>(base);
-    uint32_t* kkey = ids + n_max;                                      // [q] the set
+    uint32_t* kkey = reinterpret_cast<uint32_t*>(base);                // [q] the set (the batch is read in place)
     uint32_t* sorted = kkey + q;                                       // [p_max]
     uint16_t* kslot = reinterpret_cast<uint16_t*>(sorted + p_max);     // [n_max] set slot of every element
     uint16_t* rank_at = kslot + n_max;                                 // [q] rank of the id in a set slot
@@ -839,7 +838,7 @@ __global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int
     const int mo = batch_map_off(c, b, begin);
     const uint32_t qmask = (uint32_t)q - 1;
     const int qbits = ilog2((uint32_t)q);
-    for (int i = lane; i < n; i += 32) ids[i] = __ldg(c.idx + begin + i);
+    const uint32_t* __restrict__ ids = c.idx + begin;
     for (int i = lane; i < q; i += 32) kkey[i] = kEmpty;
     __syncwarp();
     int fresh = 0;
@@ -847,7 +846,7 @@ __global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int
     for (int i0 = 0; i0 < n; i0 += 32) {
         const int i = i0 + lane;
         if (i < n) {
-            const uint32_t id = ids[i];
+            const uint32_t id = __ldg(ids + i);
             uint32_t h = (id * 0x9E3779B1u) >> (32 - qbits);
             for (;;) {
                 const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
@@ -1060,8 +1059,9 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
     const int b = blockIdx.x * warps + wid;
     if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
     unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
-    uint32_t* ids = reinterpret_cast<uint32_t*>(base);
-    uint32_t* kkey = ids + n_max;
+    // (the batch itself is not copied: its indices are read where they lie, through L1 -- the 4 KB per warp
+    // decide how many warps an SM holds, and this kernel lives on occupancy)
+    uint32_t* kkey = reinterpret_cast<uint32_t*>(base);
     uint32_t* kpos = kkey + q;
     uint32_t* tpos = kpos + q;
     uint16_t* rank_of = reinterpret_cast<uint16_t*>(tpos + c.table_size);
@@ -1075,7 +1075,7 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
     const uint32_t tsize = c.table_size, tmask = tsize - 1;
     const uint32_t qmask = (uint32_t)q - 1;
     const int qbits = ilog2((uint32_t)q);
-    for (int i = lane; i < n; i += 32) ids[i] = __ldg(c.idx + begin + i);
+    const uint32_t* __restrict__ ids = c.idx + begin;
     for (int i = lane; i < q; i += 32) { kkey[i] = kEmpty; kpos[i] = kEmpty; }
     for (int i = lane; i < (int)tsize; i += 32) tpos[i] = kEmpty;
     __syncwarp();
@@ -1085,7 +1085,7 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
     for (int i0 = 0; i0 < n; i0 += 32) {
         const int i = i0 + lane;
         if (i < n && !overflow) {
-            const uint32_t id = ids[i];
+            const uint32_t id = __ldg(ids + i);
             uint32_t h = (id * 0x9E3779B1u) >> (32 - qbits);
             for (;;) {
                 const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
@@ -1136,7 +1136,7 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
     __syncwarp();
     for (int w0 = 0; w0 < nu; w0 += 32) {
         uint32_t cur = (w0 + lane < nu) ? (uint32_t)rank_of[w0 + lane] : kEmpty;
-        uint32_t h = cur != kEmpty ? hash_slot(ids[cur], c.multiplier, c.table_bits) : 0u;
+        uint32_t h = cur != kEmpty ? hash_slot(__ldg(ids + cur), c.multiplier, c.table_bits) : 0u;
         uint32_t taken = kEmpty;  // slot this lane turned from empty to occupied
         while (__any_sync(0xffffffffu, cur != kEmpty)) {
             if (cur != kEmpty) {
@@ -1169,7 +1169,7 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
         if (p != kEmpty) {
             const int rk = run + __popc(occ & ((1u << lane) - 1));
             rank_of[s] = (uint16_t)rk;
-            suid[rk] = ids[p];
+            suid[rk] = __ldg(ids + p);
             kpos[kslot[p]] = (uint32_t)s;
         }
         run += __popc(occ);
@@ -1180,7 +1180,7 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
     uint16_t* __restrict__ amap = c.out.d_assembly_map ? c.out.d_assembly_map + mo : nullptr;
     for (int i = lane; i < n; i += 32) {
         const uint32_t s = kpos[kslot[i]];
-        const uint32_t h0 = hash_slot(ids[i], c.multiplier, c.table_bits);
+        const uint32_t h0 = hash_slot(__ldg(ids + i), c.multiplier, c.table_bits);
         const int chain = (int)((s - h0) & tmask) + 1;
         csum += chain;
         cmax = max(cmax, chain);
@@ -1968,9 +1968,9 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             // one warp per batch (distinct ids, then a sort of those only) when its tables fit; else the CTA sort
             const int u_bound = c.enforce_budget && cfg->max_unique < max_span ? cfg->max_unique : max_span;
             const int wn = (max_span + 31) & ~31;
-            const int wq = (int)next_pow2((uint32_t)(2 * (u_bound + 32)));
+            const int wq = (int)next_pow2((uint32_t)((u_bound + 32) * 3 / 2 + 2));  // the set holds <= u_bound + 32 ids
             const int wp = (int)next_pow2((uint32_t)(u_bound + 32));
-            const int per_warp = (wn * 4 + wq * 4 + wp * 4 + wn * 2 + wq * 2 + 15) & ~15;
+            const int per_warp = (wq * 4 + wp * 4 + wn * 2 + wq * 2 + 15) & ~15;
             // (a few long batches -- configs[0]: 509 batches of 768 -- do not fill the GPU with one warp each:
             // the CTA sort is faster there)
             const bool few_long = nb < 2048 && wp > 512;
@@ -1987,8 +1987,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             // one warp per batch when a warp's tables fit comfortably; else one CTA per batch
             const int u_bound = (uint32_t)max_span < hc.table_size ? max_span : (int)hc.table_size;
             const int wn = (max_span + 31) & ~31;
-            const int wq = (int)next_pow2((uint32_t)(2 * (u_bound + 1) + 64));
-            const int per_warp = (wn * 4 + wq * 8 + (int)hc.table_size * 6 + wn * 2 + ((int)hc.table_size >> 3) + 4 + 15) & ~15;
+            const int wq = (int)next_pow2((uint32_t)((u_bound + 32) * 3 / 2 + 2));  // the set holds <= u_bound + 32 ids: load <= 2/3
+            const int per_warp = (wq * 8 + (int)hc.table_size * 6 + wn * 2 + ((int)hc.table_size >> 3) + 4 + 15) & ~15;
             if (per_warp <= 24 * 1024 && hc.table_size <= 4096) {
                 int warps = 8;
                 while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
