@@ -7,6 +7,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvrgeom.so")
+ABI_VERSION = 2  # VRGEOM_ABI_VERSION of include/vrgeom.h this binding was written against
 
 VR_NAIVE, VR_WARP, VR_SORT, VR_HASH, VR_PHASH = range(5)
 STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_HASH, "phash": VR_PHASH}
@@ -108,7 +109,7 @@ def lib():
             fn = getattr(handle, name)
             fn.restype = res
             fn.argtypes = args
-        if handle.vr_abi_version() != 2:
+        if handle.vr_abi_version() != ABI_VERSION:
             raise NativeLibraryError("libvrgeom.so ABI version mismatch")
         _lib = handle
     return _lib
