@@ -399,6 +399,57 @@ __global__ void group_scan_kernel(DynCtx c) {
     c.offsets[base] = c.n;  // batching.py:124,136: last entry = end of the final batch
 }
 
+// B3 / B4 with the table rows staged in shared memory.  Walking a chain of tables is one dependent
+// global load per step (~0.5 us each: 110 steps for the groups, 64 for the chunks of a group); here the
+// CTA copies the (exit, count) rows of `rows` consecutive tables at once -- one latency -- and thread 0
+// walks them in shared memory.
+__global__ void __launch_bounds__(1024) table_walk_kernel(DynCtx c, int level, int rows) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int* s_exit = reinterpret_cast<int*>(smem_raw);  // [rows][cap]
+    int* s_cnt = s_exit + rows * c.cap;
+    __shared__ int s_e, s_base;
+    // level 0: the groups (one CTA); level 1: the chunks of group blockIdx.x
+    const int* __restrict__ t_exit = level == 0 ? c.g_exit : c.c_exit;
+    const int* __restrict__ t_cnt = level == 0 ? c.g_cnt : c.c_cnt;
+    int k0, k1;
+    if (level == 0) { k0 = 0; k1 = c.n_groups; }
+    else { k0 = blockIdx.x * kGroup; k1 = min(c.n_chunks, k0 + kGroup); }
+    if (threadIdx.x == 0) {
+        s_e = level == 0 ? 0 : c.g_entry[blockIdx.x];
+        s_base = level == 0 ? 0 : c.g_base[blockIdx.x];
+    }
+    for (int kb = k0; kb < k1; kb += rows) {
+        const int nr = min(rows, k1 - kb);
+        const int* __restrict__ ge = t_exit + (size_t)kb * c.cap;
+        const int* __restrict__ gc = t_cnt + (size_t)kb * c.cap;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < nr * c.cap; i += blockDim.x) {  // all loads of a batch of rows in flight together
+            s_exit[i] = __ldg(ge + i);
+            s_cnt[i] = __ldg(gc + i);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int e = s_e, base = s_base;
+            for (int r = 0; r < nr; r++) {
+                if (level == 0) { c.g_entry[kb + r] = e; c.g_base[kb + r] = base; }
+                else { c.c_entry[kb + r] = e; c.c_base[kb + r] = base; }
+                base += s_cnt[r * c.cap + e];
+                e = s_exit[r * c.cap + e];
+            }
+            s_e = e;
+            s_base = base;
+        }
+        __syncthreads();
+    }
+    if (level == 0 && threadIdx.x == 0) {
+        c.g_entry[c.n_groups] = s_e;
+        c.g_base[c.n_groups] = s_base;
+        c.n_batches[0] = s_base;
+        c.n_batches[1] = 0;
+        c.offsets[s_base] = c.n;  // batching.py:124,136: last entry = end of the final batch
+    }
+}
+
 // ---- B4: true entry offset / first batch number of every chunk -----------------------------
 __global__ void __launch_bounds__(128) chunk_entry_kernel(DynCtx c) {
     const int g = blockIdx.x * blockDim.x + threadIdx.x;
@@ -554,9 +605,15 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     }
     chunk_table_kernel<<<L.n_chunks, 256, 0, stream>>>(c);
     group_table_kernel<<<L.n_groups, 256, 0, stream>>>(c);
-    group_scan_kernel<<<1, 32, 0, stream>>>(c);
+    // B3 / B4: rows of 8 tables at a time through shared memory when they fit
+    int walk_rows = 8;
+    while (walk_rows > 1 && (size_t)walk_rows * L.cap * 8 > 48 * 1024) walk_rows >>= 1;
+    const bool walk_smem = (size_t)walk_rows * L.cap * 8 <= 48 * 1024 && walk_rows >= 2 && !getenv("VR_WALK_GLOBAL");
+    if (walk_smem) table_walk_kernel<<<1, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 0, walk_rows);
+    else group_scan_kernel<<<1, 32, 0, stream>>>(c);
     if (c.draw_start) draws_check_kernel<<<(n_draws + 256) / 256, 256, 0, stream>>>(c);
-    chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
+    if (walk_smem) table_walk_kernel<<<L.n_groups, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 1, walk_rows);
+    else chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
     emit_offsets_kernel<<<(int)ceil_div(L.n_chunks, 128), 128, 0, stream>>>(c);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
