@@ -154,28 +154,35 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
         cnt[i] = 0;
     }
     __syncthreads();
-    // insert + count (the ids of four positions are loaded ahead of their insertions)
-    for (int r0 = t; r0 < np; r0 += 4 * kLinkThreads) {
-        uint32_t idv[4];
-#pragma unroll
-        for (int u = 0; u < 4; u++) idv[u] = r0 + u * kLinkThreads < np ? c.ids[hs + r0 + u * kLinkThreads] : 0u;
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-            const int r = r0 + u * kLinkThreads;
-            if (r >= np) break;
-            const uint32_t id = idv[u];
-            // double hashing over a power-of-two table (odd step): at load 0.75 an insertion takes ~2 probes on
-            // average and the longest chain among the 32 lanes of a warp stays short; linear probing at the
-            // same load left most lanes idle behind the unluckiest one (ncu: 13 of 32 lanes active)
-            uint32_t h = (id * 0x9E3779B1u) >> shift;
-            const uint32_t step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
-            for (;;) {
+    // insert + count.  Every thread owns the positions t, t + 256, ... and inserts them as a per-lane STATE
+    // MACHINE: one probe per trip; a lane whose probe resolves moves straight on to its next position
+    // instead of waiting for the longest chain among the 32 lanes.  The loop then runs max-over-lanes of
+    // the lane's TOTAL probes (~2 per position) rather than the sum of per-position maxima (~8 each;
+    // ncu: 15 of 32 lanes active in the probe loop before).  The next position's id is loaded one ahead.
+    {
+        int r = t;
+        bool active = r < np;
+        uint32_t id = active ? c.ids[hs + r] : 0u;
+        uint32_t id_next = r + kLinkThreads < np ? c.ids[hs + r + kLinkThreads] : 0u;
+        // double hashing over a power-of-two table (odd step)
+        uint32_t h = (id * 0x9E3779B1u) >> shift;
+        uint32_t step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
+        while (__any_sync(0xffffffffu, active)) {
+            if (active) {
                 const uint32_t k = atomicCAS(&keys[h], kEmpty, id);
-                if (k == kEmpty || k == id) break;
-                h = (h + step) & mask;
+                if (k == kEmpty || k == id) {
+                    slot_of[r] = (uint16_t)h;
+                    atomicAdd(&cnt[h], 1u);
+                    r += kLinkThreads;
+                    active = r < np;
+                    id = id_next;
+                    if (r + kLinkThreads < np) id_next = c.ids[hs + r + kLinkThreads];
+                    h = (id * 0x9E3779B1u) >> shift;
+                    step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
+                } else {
+                    h = (h + step) & mask;
+                }
             }
-            slot_of[r] = (uint16_t)h;
-            atomicAdd(&cnt[h], 1u);
         }
     }
     __syncthreads();
