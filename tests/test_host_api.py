@@ -200,3 +200,34 @@ def test_runner_validation_is_host_side():
     stream, rep, stats = P.run_on_indices("hash", np.array([], dtype=np.uint32), [], BatchConfig(),
                                           P.identity_shader(), HashConfig())
     assert len(stream) == 0 and rep.invocations == 0 and stats.total == 0
+
+
+def test_scene_corpus_is_the_config5_recipe():
+    """rng = default_rng(2018), kind = k % 4 (grid, icosphere, shuffled grid, shuffled
+    icosphere), sizes drawn before the shuffle seed.  Pinned on the first 40 draws; the 1000-draw totals
+    (20 397 942 triangles, 10 319 577 vertices) are asserted by the GPU scale test."""
+    from paper_1805_08893_b200.draws import scene_corpus
+    ms = scene_corpus(40)
+    assert sum(m.triangle_count for m in ms) == 799_986 and sum(m.vertex_count for m in ms) == 404_742
+    assert [m.triangle_count for m in ms[:8]] == [22698, 5120, 12118, 5120, 12480, 20480, 16102, 5120]
+    assert list(ms[2].indices[:6]) == [2815, 2889, 2816, 916, 989, 990]    # shuffled grid
+    assert list(ms[3].indices[:6]) == [346, 1353, 1352, 274, 1062, 1067]  # shuffled icosphere
+    again = scene_corpus(40)
+    assert all(np.array_equal(a.indices, b.indices) for a, b in zip(ms, again))
+
+
+def test_oracle_draws_helper_concatenates_per_mesh_runs():
+    """The multi-draw parity tests compare against per-mesh oracle runs glued together; check the glue on
+    two tiny meshes against a hand-built expectation."""
+    import oracle as O
+    from helpers import oracle_draws
+    import paper_1805_08893_b200 as P
+    a, b = P.gen_grid(3, 3), P.gen_grid(2, 4)
+    got = oracle_draws(O, "sort", [a, b], shade=False)
+    fa = O.run("sort", a.indices, [0], [len(a.indices)])
+    fb = O.run("sort", b.indices, [0], [len(b.indices)])
+    assert list(got["offsets"]) == [0, len(a.indices), len(a.indices) + len(b.indices)]
+    assert np.array_equal(got["flat"]["unique_ids"], np.concatenate([fa.unique_ids, fb.unique_ids]))
+    assert list(got["flat"]["round_uid_off"]) == [0, fa.invocations, fa.invocations + fb.invocations]
+    assert got["per_draw"] == [(1, fa.invocations), (1, fb.invocations)]
+    assert got["totals"]["invocations"] == fa.invocations + fb.invocations
