@@ -91,3 +91,60 @@ def test_two_rank_statistics_match_single_process():
     assert total[N.VR_STAT_PROBES_FAST] == fr.probes_fast
     assert total[N.VR_STAT_PROBE_MAX_CHAIN] == fr.probe_max_chain
     assert total[N.VR_STAT_ERROR] == -1
+
+
+def _draw_worker(rank, world, port, q):
+    """Multi-draw scene sharded by whole draws: every rank runs the per-mesh path over the
+    draws lpt_assign gives it; the reduced statistics must equal the single-process scene."""
+    import oracle as O
+    from paper_1805_08893_b200.draws import scene_corpus
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    meshes = scene_corpus(14, seed=5, lo=6, hi=24, ico=(1, 3))
+    mine = shard.lpt_assign([m.triangle_count for m in meshes], world)[rank]
+    stats = torch.zeros(N.VR_STATS_WORDS, dtype=torch.int64)
+    stats[N.VR_STAT_ERROR] = -1
+    for d in mine:
+        idx = meshes[int(d)].indices
+        offs = O.dynamic_batches(idx, max_unique=32, max_indices=127)
+        fr = O.run("hash", idx, offs[:-1], offs[1:], max_unique=32, table_size=32)
+        stats[N.VR_STAT_INDICES] += fr.indices
+        stats[N.VR_STAT_INVOCATIONS] += fr.invocations
+        stats[N.VR_STAT_BATCHES] += len(offs) - 1
+        stats[N.VR_STAT_ROUNDS] += fr.rounds
+        stats[N.VR_STAT_PROBES_FAST] += fr.probes_fast
+        stats[N.VR_STAT_PROBE_MAX_CHAIN] = max(int(stats[N.VR_STAT_PROBE_MAX_CHAIN]), fr.probe_max_chain)
+    total = shard.reduce_stats(stats)
+    if rank == 0:
+        q.put((total.tolist(), [int(x) for x in mine]))
+    dist.destroy_process_group()
+
+
+def test_two_rank_draw_sharding_matches_single_process():
+    import oracle as O
+    from paper_1805_08893_b200.draws import scene_corpus
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_draw_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    total, mine0 = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    meshes = scene_corpus(14, seed=5, lo=6, hi=24, ico=(1, 3))
+    parts = shard.lpt_assign([m.triangle_count for m in meshes], world)
+    assert sorted(int(x) for p in parts for x in p) == list(range(14)) and mine0 == [int(x) for x in parts[0]]
+    loads = [sum(meshes[int(d)].triangle_count for d in p) for p in parts]
+    assert max(loads) - min(loads) <= max(m.triangle_count for m in meshes)  # LPT bound
+    want = dict(i=0, v=0, b=0, r=0, p=0, c=0)
+    for m in meshes:
+        offs = O.dynamic_batches(m.indices, max_unique=32, max_indices=127)
+        fr = O.run("hash", m.indices, offs[:-1], offs[1:], max_unique=32, table_size=32)
+        want["i"] += fr.indices; want["v"] += fr.invocations; want["b"] += len(offs) - 1
+        want["r"] += fr.rounds; want["p"] += fr.probes_fast; want["c"] = max(want["c"], fr.probe_max_chain)
+    assert (total[N.VR_STAT_INDICES], total[N.VR_STAT_INVOCATIONS], total[N.VR_STAT_BATCHES]) == (want["i"], want["v"], want["b"])
+    assert (total[N.VR_STAT_ROUNDS], total[N.VR_STAT_PROBES_FAST], total[N.VR_STAT_PROBE_MAX_CHAIN]) == (want["r"], want["p"], want["c"])
+    assert total[N.VR_STAT_ERROR] == -1
