@@ -20,6 +20,12 @@
 //           compose associatively, so the chain is resolved by a reduce-then-scan over chunk
 //           tables (B1 chunk tables, B2 group tables, B3 group scan, B4 chunk entries) and
 //           B5 writes the offsets array (batching.py:128-137).
+//
+// Kernel choice (vr_dynamic_batches_draws below): batch windows up to ~4000 indices take the tile link
+// kernel (A1), the shared-memory window walk (A2) and the shared-memory chain walks (B3/B4); longer
+// windows fall back to the warp-synchronous link kernel and the global-memory walks.  Ablation knobs
+// (environment, read per call): VR_LINKS_WARP=1, VR_GREEDY_GLOBAL=1, VR_WALK_GLOBAL=1 force the fallbacks;
+// VR_LINK_TILE=<positions>, VR_GREEDY_RUN=<primitives> resize the tile / the per-thread run of the fallback.
 #include "vr_common.cuh"
 
 namespace vr {
