@@ -335,3 +335,23 @@ def test_dynamic_adversarial_streams(cuda_lib):
             want = O.dynamic_batches(ids, primitive_size=ps, max_unique=cfg.max_unique, max_indices=cfg.max_indices)
             got = engine.dynamic_offsets_device(ids, cfg).cpu().numpy().astype(np.int64)
             assert np.array_equal(got, want), f"{name} {kw}: first difference at batch {int(np.argmax(got[:len(want)] != want[:len(got)]))}"
+
+
+def test_fallback_kernels_agree(cuda_lib, monkeypatch):
+    """The kernels kept for long batch windows / few long batches (warp-synchronous links, global-memory
+    walks, CTA sort) are forced through their ablation knobs and must give the same bytes."""
+    mesh = P.shuffle_triangles(P.gen_grid(150, 130), 4)
+    cfg = BatchConfig()
+
+    def once():
+        offs = engine.dynamic_offsets_device(mesh.indices, cfg)
+        run = engine.run_device("sort", engine.to_device_indices(mesh.indices), offs[:-1], offs[1:], offs.numel() - 1,
+                                len(mesh.indices), 1023, cfg, None, engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
+        return offs.cpu().numpy(), run.flat()
+
+    offs_a, flat_a = once()
+    for k in ("VR_LINKS_WARP", "VR_GREEDY_GLOBAL", "VR_WALK_GLOBAL", "VR_SORT_CTA"):
+        monkeypatch.setenv(k, "1")
+    offs_b, flat_b = once()
+    assert np.array_equal(offs_a, offs_b) and np.array_equal(offs_a.astype(np.int64), O.dynamic_batches(mesh.indices))
+    assert_flat_equal(flat_a, flat_b, "fallback kernels")
