@@ -1205,9 +1205,9 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
 // warp_width slots every element probes at most max_fast_probes slots of a table that already
 // holds the group's earlier insertions, then the deferred elements are inserted one at a time by
 // scanning warp_width-slot windows.  One WARP per batch: the batch, the table and the slot map
-// live in shared memory, lane 0 replays the reference's order of events literally (exactness
-// first: SURVEY.md 8f-1), all lanes stage the batch and produce the outputs (occupied slots
-// ranked in table order, strategies.py:370-380).
+// live in shared memory; the elements are replayed in the reference's order, one at a time, and the
+// probes of one element are examined by the lanes in parallel (see below); all lanes stage the batch and
+// produce the outputs (occupied slots ranked in table order, strategies.py:370-380).
 // ---------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, int w, int mfp, int per_warp_bytes) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1237,55 +1237,81 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
     int status = VR_OK;
     long long fast = 0, slow = 0;
     int max_chain = 0;
-    if (lane == 0) {
-        for (int gb = 0; gb < n && status == VR_OK; gb += w) {  // strategies.py:321
-            int nd = 0;
-            const int top = min(gb + w, n);
-            for (int i = gb; i < top; i++) {
-                const uint32_t vid = ids[i];
-                uint32_t p = hash_slot(vid, c.multiplier, c.table_bits);
-                int chain = 0, resolved = -1;
-                while (chain < mfp) {  // :328
-                    chain++;
-                    if (!occ[p]) { occ[p] = 1; tab[p] = vid; resolved = (int)p; break; }
-                    if (tab[p] == vid) { resolved = (int)p; break; }
-                    p = p + 1 == tsize ? 0 : p + 1;
-                }
-                fast += chain;
-                if (resolved >= 0) {
-                    slot_map[i] = (uint16_t)resolved;
-                    max_chain = max(max_chain, chain);
-                } else {
-                    d_i[nd] = i; d_p[nd] = (int)p; d_chain[nd] = chain; nd++;
+    // The reference's order of events is kept element by element (every element sees the table exactly as
+    // the sequential emulation leaves it), but the PROBES of one element -- up to max_fast_probes slots, then
+    // warp_width-slot windows -- are looked at by the lanes side by side: the table does not change while one
+    // element probes, so "first slot that is free or holds the id" is a ballot + ffs instead of a chain of
+    // dependent shared-memory loads.  All variables below are warp-uniform.
+    for (int gb = 0; gb < n && status == VR_OK; gb += w) {  // strategies.py:321
+        int nd = 0;
+        const int top = min(gb + w, n);
+        for (int i = gb; i < top; i++) {
+            const uint32_t vid = ids[i];
+            const uint32_t p0 = hash_slot(vid, c.multiplier, c.table_bits);
+            int chain = mfp, resolved = -1;
+            for (int k0 = 0; k0 < mfp; k0 += 32) {  // :328, 32 probes at a time
+                const int k = k0 + lane;
+                const uint32_t sl = (p0 + (uint32_t)k) % tsize;
+                const bool in = k < mfp;
+                const bool fr = in && !occ[sl];
+                const bool hit = in && !fr && tab[sl] == vid;
+                const uint32_t stop = __ballot_sync(0xffffffffu, fr || hit);
+                if (stop) {
+                    const int first = __ffs((int)stop) - 1;
+                    chain = k0 + first + 1;
+                    resolved = (int)((p0 + (uint32_t)(k0 + first)) % tsize);
+                    if (lane == first && fr) { occ[sl] = 1; tab[sl] = vid; }
+                    break;
                 }
             }
-            for (int d = 0; d < nd && status == VR_OK; d++) {  // :345
-                const int i = d_i[d];
-                uint32_t p = (uint32_t)d_p[d];
-                int chain = d_chain[d];
-                const uint32_t vid = ids[i];
-                long long scanned = 0;
-                for (;;) {
-                    if (scanned > (long long)tsize + w) { status = VR_ERR_HASH_FULL; break; }  // :348-349
-                    slow += w;  // :351
-                    int pos = 0;
-                    for (int l = 0; l < w; l++) {  // ballot + ffs over the window
-                        const uint32_t sl = (p + (uint32_t)l) % tsize;
-                        if (!occ[sl] || tab[sl] == vid) { pos = l + 1; break; }
-                    }
-                    if (pos) {
-                        const uint32_t sl = (p + (uint32_t)(pos - 1)) % tsize;
-                        if (!occ[sl]) { occ[sl] = 1; tab[sl] = vid; }
-                        slot_map[i] = (uint16_t)sl;
-                        max_chain = max(max_chain, chain + pos);
-                        break;
-                    }
-                    p = (p + (uint32_t)w) % tsize;
-                    chain += w;
-                    scanned += w;
-                }
+            __syncwarp();
+            fast += chain;
+            if (resolved >= 0) {
+                if (lane == 0) slot_map[i] = (uint16_t)resolved;
+                max_chain = max(max_chain, chain);
+            } else {
+                if (lane == 0) { d_i[nd] = i; d_p[nd] = (int)((p0 + (uint32_t)mfp) % tsize); d_chain[nd] = mfp; }
+                nd++;
             }
         }
+        __syncwarp();
+        for (int d = 0; d < nd && status == VR_OK; d++) {  // :345
+            const int i = d_i[d];
+            uint32_t p = (uint32_t)d_p[d];
+            int chain = d_chain[d];
+            const uint32_t vid = ids[i];
+            long long scanned = 0;
+            for (;;) {
+                if (scanned > (long long)tsize + w) { status = VR_ERR_HASH_FULL; break; }  // :348-349
+                slow += w;  // :351
+                int pos = 0;
+                uint32_t psl = 0;
+                for (int l0 = 0; l0 < w && !pos; l0 += 32) {  // ballot + ffs over the window
+                    const int l = l0 + lane;
+                    const uint32_t sl = (p + (uint32_t)l) % tsize;
+                    const bool in = l < w;
+                    const bool fr = in && !occ[sl];
+                    const bool hit = in && !fr && tab[sl] == vid;
+                    const uint32_t stop = __ballot_sync(0xffffffffu, fr || hit);
+                    if (stop) {
+                        const int first = __ffs((int)stop) - 1;
+                        pos = l0 + first + 1;
+                        psl = (p + (uint32_t)(pos - 1)) % tsize;
+                        if (lane == first && fr) { occ[sl] = 1; tab[sl] = vid; }
+                    }
+                }
+                __syncwarp();
+                if (pos) {
+                    if (lane == 0) slot_map[i] = (uint16_t)psl;
+                    max_chain = max(max_chain, chain + pos);
+                    break;
+                }
+                p = (p + (uint32_t)w) % tsize;
+                chain += w;
+                scanned += w;
+            }
+        }
+        __syncwarp();
     }
     status = __shfl_sync(0xffffffffu, status, 0);
     __syncwarp();
