@@ -1215,7 +1215,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
     const int warps = blockDim.x >> 5;
     const int b = blockIdx.x * warps + wid;
     if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
-    const uint32_t tsize = c.table_size;
+    const uint32_t tsize = c.table_size, tmask = tsize - 1;  // a power of two (HashConfig, strategies.py:78-80)
     unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
     uint32_t* ids = reinterpret_cast<uint32_t*>(base);
     uint32_t* tab = ids + n_max;                                        // [tsize] ids
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
             int chain = mfp, resolved = -1;
             for (int k0 = 0; k0 < mfp; k0 += 32) {  // :328, 32 probes at a time
                 const int k = k0 + lane;
-                const uint32_t sl = (p0 + (uint32_t)k) % tsize;
+                const uint32_t sl = (p0 + (uint32_t)k) & tmask;
                 const bool in = k < mfp;
                 const bool fr = in && !occ[sl];
                 const bool hit = in && !fr && tab[sl] == vid;
@@ -1259,7 +1259,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
                 if (stop) {
                     const int first = __ffs((int)stop) - 1;
                     chain = k0 + first + 1;
-                    resolved = (int)((p0 + (uint32_t)(k0 + first)) % tsize);
+                    resolved = (int)((p0 + (uint32_t)(k0 + first)) & tmask);
                     if (lane == first && fr) { occ[sl] = 1; tab[sl] = vid; }
                     break;
                 }
@@ -1270,7 +1270,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
                 if (lane == 0) slot_map[i] = (uint16_t)resolved;
                 max_chain = max(max_chain, chain);
             } else {
-                if (lane == 0) { d_i[nd] = i; d_p[nd] = (int)((p0 + (uint32_t)mfp) % tsize); d_chain[nd] = mfp; }
+                if (lane == 0) { d_i[nd] = i; d_p[nd] = (int)((p0 + (uint32_t)mfp) & tmask); d_chain[nd] = mfp; }
                 nd++;
             }
         }
@@ -1288,7 +1288,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
                 uint32_t psl = 0;
                 for (int l0 = 0; l0 < w && !pos; l0 += 32) {  // ballot + ffs over the window
                     const int l = l0 + lane;
-                    const uint32_t sl = (p + (uint32_t)l) % tsize;
+                    const uint32_t sl = (p + (uint32_t)l) & tmask;
                     const bool in = l < w;
                     const bool fr = in && !occ[sl];
                     const bool hit = in && !fr && tab[sl] == vid;
@@ -1296,7 +1296,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
                     if (stop) {
                         const int first = __ffs((int)stop) - 1;
                         pos = l0 + first + 1;
-                        psl = (p + (uint32_t)(pos - 1)) % tsize;
+                        psl = (p + (uint32_t)(pos - 1)) & tmask;
                         if (lane == first && fr) { occ[sl] = 1; tab[sl] = vid; }
                     }
                 }
@@ -1306,7 +1306,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
                     max_chain = max(max_chain, chain + pos);
                     break;
                 }
-                p = (p + (uint32_t)w) % tsize;
+                p = (p + (uint32_t)w) & tmask;
                 chain += w;
                 scanned += w;
             }
