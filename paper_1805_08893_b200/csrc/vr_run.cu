@@ -1217,8 +1217,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
     if (b >= c.n_batches || c.acc[ACC_ABORT]) return;
     const uint32_t tsize = c.table_size, tmask = tsize - 1;  // a power of two (HashConfig, strategies.py:78-80)
     unsigned char* base = smem_raw + (size_t)wid * per_warp_bytes;
-    uint32_t* ids = reinterpret_cast<uint32_t*>(base);
-    uint32_t* tab = ids + n_max;                                        // [tsize] ids
+    uint32_t* tab = reinterpret_cast<uint32_t*>(base);                  // [tsize] ids (the batch is read in place)
     int32_t* d_i = reinterpret_cast<int32_t*>(tab + tsize);             // deferred elements of a group: index,
     int32_t* d_p = d_i + 64;                                            //   slot where fast probing stopped,
     int32_t* d_chain = d_p + 64;                                        //   probes so far
@@ -1231,7 +1230,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
         return;
     }
     const int mo = batch_map_off(c, b, begin);
-    for (int i = lane; i < n; i += 32) ids[i] = __ldg(c.idx + begin + i);
+    const uint32_t* __restrict__ ids = c.idx + begin;
     for (int s = lane; s < (int)tsize; s += 32) occ[s] = 0;
     __syncwarp();
     int status = VR_OK;
@@ -1246,7 +1245,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
         int nd = 0;
         const int top = min(gb + w, n);
         for (int i = gb; i < top; i++) {
-            const uint32_t vid = ids[i];
+            const uint32_t vid = __ldg(ids + i);
             const uint32_t p0 = hash_slot(vid, c.multiplier, c.table_bits);
             int chain = mfp, resolved = -1;
             for (int k0 = 0; k0 < mfp; k0 += 32) {  // :328, 32 probes at a time
@@ -1279,7 +1278,7 @@ __global__ void __launch_bounds__(256) phash_warp_kernel(RunCtx c, int n_max, in
             const int i = d_i[d];
             uint32_t p = (uint32_t)d_p[d];
             int chain = d_chain[d];
-            const uint32_t vid = ids[i];
+            const uint32_t vid = __ldg(ids + i);
             long long scanned = 0;
             for (;;) {
                 if (scanned > (long long)tsize + w) { status = VR_ERR_HASH_FULL; break; }  // :348-349
@@ -1983,7 +1982,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             if (st) return st;
         } else if (strategy == VR_PHASH) {
             const int wn = (max_span + 3) & ~3;
-            const int per_warp = (wn * 4 + (int)hc.table_size * 4 + 3 * 64 * 4 + wn * 2 + (int)hc.table_size * 2 + (int)hc.table_size + 15) & ~15;
+            const int per_warp = ((int)hc.table_size * 4 + 3 * 64 * 4 + wn * 2 + (int)hc.table_size * 2 + (int)hc.table_size + 15) & ~15;
             if (per_warp > 200 * 1024) return VR_ERR_UNSUPPORTED;
             int warps = 8;
             while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
