@@ -41,7 +41,7 @@ WORKLOADS = {
     "c4_hash": dict(desc="configs[3]: shuffle_triangles(gen_grid(1898,1898), 0), dynamic 256/1023, hash 256",
                     side=1898, shuffle=0, strategy="hash", batching="dynamic",
                     expect=dict(batches=84672, rounds=84672, invocations=21591005, probes_fast=216377586)),
-    "c4_phash": dict(desc="configs[3] mesh, dynamic 256/1023, two-tier hash 256 (exactness row, lane 0 replays the reference)",
+    "c4_phash": dict(desc="configs[3] mesh, dynamic 256/1023, two-tier hash 256 (elements replayed in the reference's order, probes of an element in parallel)",
                      side=1898, shuffle=0, strategy="phash", batching="dynamic",
                      expect=dict(batches=84672, rounds=84672, invocations=21591005)),
     "c4_sort": dict(desc="configs[3] mesh, dynamic 256/1023, sort dedup",
