@@ -19,14 +19,22 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;  // mesh.py:11-13: reserved, never a ve
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline uint32_t next_pow2(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));  // (the kernels call this once per batch)
+#else
     uint32_t p = 1;
     while (p < x) p <<= 1;
     return p;
+#endif
 }
 __host__ __device__ inline int ilog2(uint32_t pow2) {
+#ifdef __CUDA_ARCH__
+    return pow2 <= 1 ? 0 : 32 - __clz(pow2 - 1);
+#else
     int b = 0;
     while ((1u << b) < pow2) b++;
     return b;
+#endif
 }
 
 // strategies.py:88-91 HashConfig.slot; bits == 0 (table_size 1) -> slot 0.
