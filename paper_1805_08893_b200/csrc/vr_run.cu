@@ -856,9 +856,7 @@ __global__ void __launch_bounds__(256) sort_warp_kernel(RunCtx c, int n_max, int
             }
             kslot[i] = (uint16_t)h;
         }
-        int tot = fresh;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+        const int tot = __reduce_add_sync(0xffffffffu, fresh);  // one REDUX instead of five shuffles
         if (tot > u_bound) { overflow = true; break; }  // uniform: stop before the set can fill up
     }
     if (overflow) {  // only under the unique budget: more distinct ids than max_unique (strategies.py:451-455)
@@ -1096,15 +1094,11 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
             atomicMin(&kpos[h], (uint32_t)i);
             kslot[i] = (uint16_t)h;
         }
-        int tot = fresh;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, d);
+        const int tot = __reduce_add_sync(0xffffffffu, fresh);  // one REDUX instead of five shuffles
         overflow = tot > u_bound;  // uniform: stop before the set can fill up
         if (overflow) break;
     }
-    int nu = fresh;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) nu += __shfl_xor_sync(0xffffffffu, nu, d);
+    const int nu = __reduce_add_sync(0xffffffffu, fresh);
     if (overflow || nu > (int)tsize) {
         // more unique ids than table slots: the reference's chain would exceed table_size (strategies.py:283-284)
         if (lane == 0) {
