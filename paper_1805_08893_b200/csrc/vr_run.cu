@@ -1180,11 +1180,8 @@ __global__ void __launch_bounds__(256) hash_warp_kernel(RunCtx c, int n_max, int
         cmax = max(cmax, chain);
         if (amap) amap[i] = rank_of[s];
     }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        csum += __shfl_xor_sync(0xffffffffu, csum, d);
-        cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, d));
-    }
+    csum = __reduce_add_sync(0xffffffffu, csum);
+    cmax = __reduce_max_sync(0xffffffffu, cmax);
     if (lane == 0) {
         c.counts[b] = make_int2(1, nu);
         atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], (unsigned long long)csum);
