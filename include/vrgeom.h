@@ -73,7 +73,9 @@ enum vr_status {
     VR_ERR_CUDA = 11,              /* CUDA runtime failure / no device                     */
     VR_ERR_CAPACITY = 12,          /* an output buffer is smaller than the result          */
     VR_ERR_WORKSPACE = 13,         /* workspace smaller than vr_*_workspace_bytes()        */
-    VR_ERR_PRIM_OVER_BUDGET = 14   /* batching.py:119-123 ConfigError                      */
+    VR_ERR_PRIM_OVER_BUDGET = 14,  /* batching.py:119-123 ConfigError                      */
+    VR_ERR_VERTEX_RANGE = 15       /* strategies.py:62-65 positions[vid]: IndexError (an id
+                                      outside [0, vertex_count); nothing is gathered or tallied) */
 };
 
 /* batching.py:23-61 BatchConfig (same fields, same defaults: 96/256/1023/32/256/3) */

@@ -14,7 +14,8 @@ STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_
 
 (VR_OK, VR_ERR_UNKNOWN_STRATEGY, VR_ERR_BAD_BATCH, VR_ERR_TABLE_BELOW_BUDGET, VR_ERR_OVER_BUDGET,
  VR_ERR_HASH_FULL, VR_ERR_WARP_NO_PROGRESS, VR_ERR_WARP_WIDTH, VR_ERR_UNALIGNED, VR_ERR_BAD_CONFIG,
- VR_ERR_UNSUPPORTED, VR_ERR_CUDA, VR_ERR_CAPACITY, VR_ERR_WORKSPACE, VR_ERR_PRIM_OVER_BUDGET) = range(15)
+ VR_ERR_UNSUPPORTED, VR_ERR_CUDA, VR_ERR_CAPACITY, VR_ERR_WORKSPACE, VR_ERR_PRIM_OVER_BUDGET,
+ VR_ERR_VERTEX_RANGE) = range(16)
 
 VR_FLAG_NO_BUDGET = 0x100
 VR_FLAG_CONTIGUOUS = 0x200

@@ -62,6 +62,18 @@ __device__ inline void report_error(const RunCtx& c, int64_t batch, int status) 
     long long word = (long long)(((0x7FFFFFFFFFFFLL - batch) << 8) | (long long)status);
     atomicMax(&c.acc[ACC_ERROR], word);
 }
+// Errors found after the statistics block may already have been written (shading runs behind the offset
+// scan): straight into the error word.  It is -1 when clean (init_kernel), i.e. the largest unsigned
+// value, so the minimum of (batch << 8 | status) keeps the first failing batch.
+__device__ inline void report_late_error(const RunCtx& c, int64_t batch, int status) {
+    atomicMin(reinterpret_cast<unsigned long long*>(c.out.d_stats + VR_STAT_ERROR),
+              ((unsigned long long)batch << 8) | (unsigned long long)status);
+}
+// strategies.py:62-65 positions[vid] raises for an id outside the vertex buffer; the device must neither
+// gather nor tally out of bounds.  `v` = first vertex of the batch's draw + id.
+__device__ __forceinline__ bool vertex_in_range(const ShaderParams& sp, uint32_t v) {
+    return sp.vertex_count <= 0 || v < (uint32_t)sp.vertex_count;
+}
 
 __device__ __forceinline__ int batch_map_off(const RunCtx& c, int b, int begin) {
     return c.contiguous ? begin - __ldg(c.bbegin) : c.map_off[b];
@@ -92,6 +104,7 @@ __global__ void init_kernel(RunCtx c) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the tile kernel may be scheduled; it waits below
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < ACC_WORDS) c.acc[i] = 0;
+    if (i == 0) c.out.d_stats[VR_STAT_ERROR] = -1;  // see report_late_error
     if (i < c.n_state_words) c.tile_state[i] = 0ull;
 }
 
@@ -344,7 +357,8 @@ __global__ void __launch_bounds__(kTpbThreads) warp_tpb_kernel(RunCtx c) {
 // Totals, statistics and the closing table entries (strategies.py:472-502); one thread.
 __device__ void finish_stats(const RunCtx& c, long long R, long long U) {
     int64_t* st = c.out.d_stats;
-    for (int i = 0; i < VR_STATS_WORDS; i++) st[i] = 0;
+    for (int i = 0; i < VR_STATS_WORDS; i++)
+        if (i != VR_STAT_ERROR) st[i] = 0;
     long long span_total = 0;
     if (c.n_batches > 0)
         span_total = c.contiguous ? (long long)c.bend[c.n_batches - 1] - c.bbegin[0] : c.map_off[c.n_batches];
@@ -359,11 +373,10 @@ __device__ void finish_stats(const RunCtx& c, long long R, long long U) {
     st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
     const long long e = c.acc[ACC_ERROR];
     if (e == 0) {
-        st[VR_STAT_ERROR] = -1;
         if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
         if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
     } else {
-        st[VR_STAT_ERROR] = ((0x7FFFFFFFFFFFLL - (e >> 8)) << 8) | (e & 0xFF);
+        report_late_error(c, 0x7FFFFFFFFFFFLL - (e >> 8), (int)(e & 0xFF));
         c.acc[ACC_ABORT] = 1;  // K3 must not touch the outputs
     }
 }
@@ -672,6 +685,7 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
         constexpr int U4 = 4;
         for (int j0 = 0; j0 < tot; j0 += 32 * U4) {
             uint32_t uid[U4];
+            bool live[U4];
             float4 pv[U4];
 #pragma unroll
             for (int u = 0; u < U4; u++) {
@@ -684,17 +698,20 @@ __global__ void __launch_bounds__(kFastThreads) warp_fast_kernel(RunCtx c, int b
                 const uint32_t* osrc = (const uint32_t*)__shfl_sync(0xffffffffu, my_src, owner);
                 const int j = jb + lane;
                 uid[u] = j < tot ? osrc[j - oex] : 0u;
+                live[u] = j < tot && vertex_in_range(sp, uid[u]);
+                if (j < tot && !live[u]) report_late_error(c, (int64_t)tile * T + 32 * wid + owner, VR_ERR_VERTEX_RANGE);
             }
             if (want_pos) {
 #pragma unroll
                 for (int u = 0; u < U4; u++)
-                    if (j0 + 32 * u + lane < tot) pv[u] = __ldg(sp.pos4 + uid[u]);
+                    if (live[u]) pv[u] = __ldg(sp.pos4 + uid[u]);
             }
 #pragma unroll
             for (int u = 0; u < U4; u++) {
                 const int j = j0 + 32 * u + lane;
                 if (j >= tot) continue;
                 if (want_uid) out_uid[j] = uid[u];
+                if (!live[u]) continue;
                 if (want_pos) shaded[j] = transform_position(sp, pv[u]);
                 if (want_attr)
                     for (int q = 0; q < sp.attr_words; q++)
@@ -1427,7 +1444,7 @@ constexpr int kShadeUnroll = 4;
 // (l = lane within the group): coalesced id load, 16-byte gather, transform, coalesced stores.
 template <int STRATEGY>
 __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams& sp, const uint32_t* __restrict__ src,
-                                             int cnt, int64_t dst0, int l, int width, int naive_mo, int vbase) {
+                                             int cnt, int64_t dst0, int l, int width, int naive_mo, int vbase, int batch) {
     const bool want_uid = c.out.d_unique_ids != nullptr;
     const bool want_pos = sp.kind == VR_SHADER_POSITION;
     const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
@@ -1437,23 +1454,25 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
     for (int j0 = 0; j0 < cnt; j0 += width * kShadeUnroll) {
         uint32_t uid[kShadeUnroll];
         float4 p[kShadeUnroll];
+        bool live[kShadeUnroll];
 #pragma unroll
         for (int u = 0; u < kShadeUnroll; u++) {
             const int j = j0 + u * width + l;
             uid[u] = j < cnt ? src[j] : 0u;
+            live[u] = j < cnt && vertex_in_range(sp, (uint32_t)vbase + uid[u]);
+            if (j < cnt && !live[u]) report_late_error(c, batch, VR_ERR_VERTEX_RANGE);
         }
         if (want_pos) {
 #pragma unroll
-            for (int u = 0; u < kShadeUnroll; u++) {
-                const int j = j0 + u * width + l;
-                if (j < cnt) p[u] = __ldg(sp.pos4 + vbase + uid[u]);
-            }
+            for (int u = 0; u < kShadeUnroll; u++)
+                if (live[u]) p[u] = __ldg(sp.pos4 + vbase + uid[u]);
         }
 #pragma unroll
         for (int u = 0; u < kShadeUnroll; u++) {
             const int j = j0 + u * width + l;
             if (j >= cnt) continue;
             if (want_uid) out_uid[j] = uid[u];
+            if (!live[u]) continue;
             if (want_pos) shaded[j] = transform_position(sp, p[u]);
             if (STRATEGY == VR_NAIVE && c.out.d_assembly_map) c.out.d_assembly_map[naive_mo + j] = (uint16_t)(j % c.ps);
             if (want_attr)
@@ -1510,6 +1529,7 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
         for (int j0 = 0; j0 < tot; j0 += 32 * kShadeUnroll) {
             uint32_t uid[kShadeUnroll];
             int vb[kShadeUnroll];
+            bool live[kShadeUnroll];
             float4 p[kShadeUnroll];
 #pragma unroll
             for (int u = 0; u < kShadeUnroll; u++) {
@@ -1523,17 +1543,20 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
                 vb[u] = __shfl_sync(0xffffffffu, my_vbase, owner);
                 const int j = jb + lane;
                 uid[u] = j < tot ? osrc[j - oex] : 0u;
+                live[u] = j < tot && vertex_in_range(sp, (uint32_t)vb[u] + uid[u]);
+                if (j < tot && !live[u]) report_late_error(c, 32 * s + owner, VR_ERR_VERTEX_RANGE);
             }
             if (want_pos) {
 #pragma unroll
                 for (int u = 0; u < kShadeUnroll; u++)
-                    if (j0 + 32 * u + lane < tot) p[u] = __ldg(sp.pos4 + vb[u] + uid[u]);
+                    if (live[u]) p[u] = __ldg(sp.pos4 + vb[u] + uid[u]);
             }
 #pragma unroll
             for (int u = 0; u < kShadeUnroll; u++) {
                 const int j = j0 + 32 * u + lane;
                 if (j >= tot) continue;
                 if (want_uid) out_uid[j] = uid[u];
+                if (!live[u]) continue;
                 if (want_pos) shaded[j] = transform_position(sp, p[u]);
                 if (want_attr)
                     for (int k = 0; k < sp.attr_words; k++)
@@ -1561,7 +1584,7 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
             }
             src = c.stage_uid + stage_uid_base(c, b, mo);
         }
-        shade_stream<STRATEGY>(c, sp, src, cnt.y, off.y, lane, 32, mo, sp.batch_base ? __ldg(sp.batch_base + b) : 0);
+        shade_stream<STRATEGY>(c, sp, src, cnt.y, off.y, lane, 32, mo, sp.batch_base ? __ldg(sp.batch_base + b) : 0, b);
     }
 }
 
@@ -1763,6 +1786,7 @@ const char* vr_status_string(int s) {
     case VR_ERR_CAPACITY: return "output buffer too small";
     case VR_ERR_WORKSPACE: return "workspace too small";
     case VR_ERR_PRIM_OVER_BUDGET: return "primitive has more unique indices than max_unique";
+    case VR_ERR_VERTEX_RANGE: return "index outside the vertex buffer";
     default: return "unknown status";
     }
 }

@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         }
             VR_MARK(3);
             if (active && mx >= vcount) {
-                report_error(c, b, VR_ERR_BAD_BATCH);  // index outside the vertex buffer
+                report_error(c, b, VR_ERR_VERTEX_RANGE);  // index outside the vertex buffer
                 active = false;
             }
             if (active && (claimed_begin != begin || claimed_end != begin + n)) {

@@ -61,6 +61,8 @@ def raise_status(status: int, batch: int = -1):
         raise N.NativeLibraryError(msg)
     if status in (N.VR_ERR_CAPACITY, N.VR_ERR_WORKSPACE):
         raise RuntimeError(msg)
+    if status == N.VR_ERR_VERTEX_RANGE:
+        raise IndexError(msg)  # strategies.py:62-65 positions[vid]
     raise ConfigError(msg)
 
 

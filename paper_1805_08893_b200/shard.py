@@ -1,12 +1,26 @@
 """Multi-GPU sharding of the geometry stage.
 
 Batches are independent (SPEC: "batches may be processed concurrently and results concatenated
-in batch order"), so the index stream is cut into contiguous ranges of WHOLE batches, one range
+in batch order"), so ONE index stream is cut into contiguous ranges of WHOLE batches, one range
 per rank, with the vertex buffer replicated.  No collective sits on the data path; the only
-exchange is the reduction of the statistics block (SUM for the counters, MAX for the longest
-probe chain), which is what the reference's ordered merge does (strategies.py:472-483).
-Multi-draw workloads are sharded by whole draws (longest-processing-time bin packing)."""
+exchange is one all-gather of the 16-word statistics blocks, merged locally the way the reference's
+ordered merge does (strategies.py:472-483: SUM for the counters, MAX for the longest probe chain, the
+first failing batch in stream order for the error).
+
+  static batches   cut points are multiples of batch_size: closed form, no communication
+                   (`plan_static`);
+  dynamic batches  a cut must fall on a true greedy boundary, known only after the scan: every rank
+                   runs the index-only boundary scan over the whole stream redundantly (it reads 4 B
+                   per index and writes nothing the other ranks need) and takes its slice of batches
+                   (`plan_from_offsets`; option (i) of SURVEY.md 8e);
+  multi-draw       whole draws per rank, longest-processing-time bin packing (`lpt_assign`), every rank
+                   packs and runs its own draws (`run_draws_sharded`).
+
+`run_sharded` is the per-rank entry point; `concat_flats` is the reference's ordered merge of the
+per-shard results and is what the tests compare with the unsharded run."""
 from __future__ import annotations
+
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -17,6 +31,7 @@ from . import _native as N
 SUM_WORDS = (N.VR_STAT_INDICES, N.VR_STAT_INVOCATIONS, N.VR_STAT_BATCHES, N.VR_STAT_ROUNDS,
              N.VR_STAT_PROBES_FAST, N.VR_STAT_PROBES_SLOW)
 MAX_WORDS = (N.VR_STAT_PROBE_MAX_CHAIN,)
+STAT_BATCH_BASE = 8  # spare word of the statistics block: first batch of the rank's shard (for the error merge)
 
 
 def shard_range(n_items: int, rank: int, world: int):
@@ -46,22 +61,178 @@ def lpt_assign(sizes, world: int):
     return [np.flatnonzero(owner == r) for r in range(world)]
 
 
-def reduce_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
-    """All-reduce one statistics block (int64[VR_STATS_WORDS]) across ranks; NCCL for CUDA
-    tensors, gloo for CPU tensors.  The error word takes the minimum non-negative entry."""
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
-        return stats.clone()
-    s = stats.clone()
-    summed = s.clone()
-    dist.all_reduce(summed, op=dist.ReduceOp.SUM, group=group)
-    maxed = s.clone()
-    dist.all_reduce(maxed, op=dist.ReduceOp.MAX, group=group)
-    err = s[N.VR_STAT_ERROR:N.VR_STAT_ERROR + 1].clone()
-    big = torch.full_like(err, 2**62)
-    err = torch.where(err < 0, big, err)
-    dist.all_reduce(err, op=dist.ReduceOp.MIN, group=group)
-    out = summed
+# ---------------------------------------------------------------------------------------------
+# statistics: one collective
+# ---------------------------------------------------------------------------------------------
+def merge_stats(blocks: torch.Tensor) -> torch.Tensor:
+    """[world, VR_STATS_WORDS] per-rank blocks -> the block of the whole stream (strategies.py:472-483).
+    The error word of a rank holds (batch within its shard << 8 | status); word STAT_BATCH_BASE holds the
+    shard's first batch, so the merged word names the first failing batch of the STREAM."""
+    out = torch.zeros(N.VR_STATS_WORDS, dtype=torch.int64, device=blocks.device)
+    for w in SUM_WORDS:
+        out[w] = blocks[:, w].sum()
     for w in MAX_WORDS:
-        out[w] = maxed[w]
-    out[N.VR_STAT_ERROR] = torch.where(err >= big, torch.full_like(err, -1), err)[0]
+        out[w] = blocks[:, w].max()
+    err = blocks[:, N.VR_STAT_ERROR]
+    glob = (((err >> 8) + blocks[:, STAT_BATCH_BASE]) << 8) | (err & 0xFF)
+    big = torch.full_like(err, 2 ** 62)
+    first = torch.where(err < 0, big, glob).min()
+    out[N.VR_STAT_ERROR] = torch.where(first >= 2 ** 62, torch.full_like(first, -1), first)
     return out
+
+
+def reduce_stats(stats: torch.Tensor, group=None, batch_base: int = 0) -> torch.Tensor:
+    """One statistics block per rank -> the block of the whole job, on every rank: ONE all-gather of
+    VR_STATS_WORDS int64 (NCCL for CUDA tensors, gloo for CPU tensors) and a local merge."""
+    s = stats.clone()
+    s[STAT_BATCH_BASE] = batch_base
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return merge_stats(s.unsqueeze(0))
+    world = dist.get_world_size(group)
+    parts = [torch.empty_like(s) for _ in range(world)]
+    dist.all_gather(parts, s, group=group)
+    return merge_stats(torch.stack(parts))
+
+
+# ---------------------------------------------------------------------------------------------
+# one stream, whole batches per rank
+# ---------------------------------------------------------------------------------------------
+@dataclass(frozen=True)
+class ShardPlan:
+    """This rank's contiguous range of whole batches of one stream."""
+
+    rank: int
+    world: int
+    batch_lo: int
+    batch_hi: int
+    index_lo: int
+    index_hi: int
+    static: bool
+
+    @property
+    def n_batches(self) -> int:
+        return self.batch_hi - self.batch_lo
+
+    @property
+    def span(self) -> int:
+        return self.index_hi - self.index_lo
+
+
+def plan_static(index_count: int, cfg, rank: int, world: int) -> ShardPlan:
+    """static_batches (batching.py:76-84): cut points at multiples of batch_size, no communication."""
+    nb = -(-index_count // cfg.batch_size) if index_count > 0 else 0
+    lo, hi = shard_range(nb, rank, world)
+    return ShardPlan(rank, world, lo, hi, min(lo * cfg.batch_size, index_count), min(hi * cfg.batch_size, index_count), True)
+
+
+def plan_from_offsets(offsets, rank: int, world: int) -> ShardPlan:
+    """Any offsets array (batching.py:128-137), e.g. the dynamic boundaries every rank computed for the whole
+    stream: this rank's slice of whole batches.  Reads two entries of a device array (16 bytes)."""
+    nb = max(int(offsets.shape[0]) - 1, 0)
+    lo, hi = shard_range(nb, rank, world)
+    if nb == 0:
+        return ShardPlan(rank, world, 0, 0, 0, 0, False)
+    if isinstance(offsets, torch.Tensor):
+        ends = offsets[[lo, hi]].cpu()
+        a, b = int(ends[0]), int(ends[1])
+    else:
+        a, b = int(offsets[lo]), int(offsets[hi])
+    return ShardPlan(rank, world, lo, hi, a, b, False)
+
+
+def run_sharded(strategy: str, d_indices: torch.Tensor, cfg, hcfg=None, shader=None, *, batching: str = "static",
+                offsets: torch.Tensor | None = None, rank: int | None = None, world: int | None = None,
+                want_counts: bool = False, buffers=None, group=None, plan_only: bool = False):
+    """This rank's share of ONE index stream: (DeviceRun over the rank's batches, ShardPlan).
+
+    `d_indices` is the whole stream (replicated, like the vertex buffer: 4 B per index is what a rank needs
+    to find dynamic boundaries on its own).  batching = "static" | "dynamic" | "offsets" (a precomputed
+    device offsets array for the whole stream).  The DeviceRun's outputs are relative to the shard: batch 0
+    is stream batch plan.batch_lo, the assembly map starts at index plan.index_lo."""
+    from . import engine
+
+    if rank is None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    n_idx = int(d_indices.numel())
+    dev = d_indices.device
+    if batching == "static":
+        plan = plan_static(n_idx, cfg, rank, world)
+        offs = engine.static_offsets_device(n_idx, cfg, dev) if offsets is None else offsets
+        max_span = cfg.batch_size
+    else:
+        if offsets is None:
+            if batching != "dynamic":
+                raise ValueError("batching='offsets' needs the offsets array")
+            offs = engine.dynamic_offsets_device(d_indices, cfg)  # redundant on every rank: SURVEY 8e option (i)
+        else:
+            offs = offsets
+        plan = plan_from_offsets(offs, rank, world)
+        max_span = max(cfg.batch_size, cfg.max_indices - cfg.max_indices % cfg.primitive_size)
+    if plan.n_batches == 0:
+        return None, plan
+    lo, hi = plan.batch_lo, plan.batch_hi
+    # the position-aligned (tile) kernels want a 16-byte aligned first index
+    static = plan.static and plan.index_lo % 4 == 0
+    run = engine.run_device(strategy, d_indices, offs[lo:hi], offs[lo + 1:hi + 1], hi - lo, plan.span, max_span, cfg,
+                            hcfg, shader, want_counts=want_counts, buffers=buffers, contiguous=True, static=static,
+                            plan_only=plan_only)
+    return run, plan
+
+
+def global_stats(run, plan: ShardPlan, group=None, device=None) -> torch.Tensor:
+    """Statistics of the whole stream from the per-rank runs (one all-gather).  A rank with no batches
+    contributes an empty block."""
+    if run is None:
+        s = torch.zeros(N.VR_STATS_WORDS, dtype=torch.int64, device=device or "cpu")
+        s[N.VR_STAT_ERROR] = -1
+    else:
+        s = run.stats_dev
+    return reduce_stats(s, group, batch_base=plan.batch_lo)
+
+
+def concat_flats(flats) -> dict:
+    """The reference's ordered merge (strategies.py:472-483) of per-shard flattened results, in rank order:
+    streams are concatenated, round / unique-id offsets are rebased."""
+    out = {"batch_round_off": [np.zeros(1, dtype=np.int64)], "round_uid_off": [np.zeros(1, dtype=np.int64)],
+           "round_prims": [], "unique_ids": [], "assembly_map": []}
+    extra = {}
+    r_base = u_base = 0
+    for f in flats:
+        if f is None:
+            continue
+        out["batch_round_off"].append(np.asarray(f["batch_round_off"][1:], dtype=np.int64) + r_base)
+        out["round_uid_off"].append(np.asarray(f["round_uid_off"][1:], dtype=np.int64) + u_base)
+        r_base += int(f["batch_round_off"][-1])
+        u_base += int(f["round_uid_off"][-1])
+        for k in ("round_prims", "unique_ids", "assembly_map"):
+            out[k].append(np.asarray(f[k]))
+        for k in ("shaded", "shaded_attr"):
+            if k in f:
+                extra.setdefault(k, []).append(f[k])
+        if "shade_counts" in f:  # per-vertex tallies add up (vertex buffer replicated)
+            extra["shade_counts"] = f["shade_counts"] if "shade_counts" not in extra else extra["shade_counts"] + f["shade_counts"]
+    res = {k: (np.concatenate(v) if v else np.zeros(0, dtype=np.int64)) for k, v in out.items()}
+    for k, v in extra.items():
+        res[k] = np.concatenate(v) if isinstance(v, list) else v
+    return res
+
+
+# ---------------------------------------------------------------------------------------------
+# multi-draw scenes: whole draws per rank
+# ---------------------------------------------------------------------------------------------
+def run_draws_sharded(strategy: str, meshes, cfg, hcfg=None, *, rank: int, world: int, matrix=None,
+                      want_counts: bool = False, buffers=None, device=None):
+    """BASELINE.json configs[4] across ranks: this rank packs the draws `lpt_assign` gives it (ascending draw
+    order), forms their dynamic batches and runs them.  Returns (DeviceRun or None, DrawSet or None, offsets,
+    draw ids).  Every draw restarts the greedy scan, so no boundary couples two ranks."""
+    from . import draws as D
+
+    mine = lpt_assign([len(m.indices) // cfg.primitive_size for m in meshes], world)[rank]
+    if len(mine) == 0:
+        return None, None, None, mine
+    ds = D.pack_draws([meshes[int(d)] for d in mine], device)
+    offs = D.dynamic_offsets_draws(ds, cfg)
+    run = D.run_draws(strategy, ds, offs, cfg, hcfg, matrix=matrix, want_counts=want_counts, buffers=buffers)
+    return run, ds, offs, mine

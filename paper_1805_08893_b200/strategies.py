@@ -338,8 +338,10 @@ def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: Sh
             max_span = int((be - bb).max())
             span_total = int((be - bb).sum())
             contiguous = bool((bb[1:] == be[:-1]).all())
-            static = bool(contiguous and (np.diff(bb) == cfg.batch_size).all()
-                          and (be[-1] - bb[-1]) <= cfg.batch_size and (nb == 1 or bb[1] - bb[0] == cfg.batch_size))
+            # static_batches(n, cfg) shifted to a 16-byte aligned start (the position-aligned kernels load
+            # index quads); any other equally spaced list takes the general kernels
+            static = bool(contiguous and bb[0] % 4 == 0 and (np.diff(bb) == cfg.batch_size).all()
+                          and (be[-1] - bb[-1]) <= cfg.batch_size)
 
     if strategy in ("hash", "phash"):
         hash_cfg = hash_cfg or HashConfig(table_size=cfg.block_size)  # strategies.py:431

@@ -199,9 +199,12 @@ def test_grid256_table(cuda_lib):
         if row["strategy"] == "hash":
             assert run.probes == (row["probes_fast"], 0, row["probe_max_chain"]), row
         assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), idx), row
-        if B in (32, 256):
-            h_offs = offs.cpu().numpy().astype(np.int64)
-            check_against_oracle(row["strategy"], idx, h_offs, cfg, hc, ctx=str(row))
+        # every array of every row against the oracle (all batch sizes, all strategies)
+        h_offs = offs.cpu().numpy().astype(np.int64)
+        fr = oracle_run(row["strategy"], idx, h_offs, cfg, hc)
+        assert_flat_equal(run.flat(), oracle_flat(fr), str(row))
+        if row["strategy"] in ("hash", "phash"):
+            assert run.probes == (fr.probes_fast, fr.probes_slow, fr.probe_max_chain), row
 
 
 def test_config1_headline_numbers(cuda_lib):

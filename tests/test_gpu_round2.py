@@ -1,0 +1,95 @@
+"""Round-2 parity additions: out-of-range vertex ids on every kernel path, static-looking batch lists that
+do not start on an index quad, the stream dump format."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1805_08893_b200 as P
+from helpers import MATRIX, assert_flat_equal, oracle_flat
+from paper_1805_08893_b200 import _native as N
+from paper_1805_08893_b200 import engine
+from paper_1805_08893_b200.batching import Batch, BatchConfig
+from paper_1805_08893_b200.strategies import HashConfig
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("strategy", ["naive", "warp", "sort", "hash", "phash"])
+@pytest.mark.parametrize("shader", ["position", "identity"])
+def test_vertex_id_outside_buffer_every_strategy(cuda_lib, strategy, shader):
+    """strategies.py:62-65: positions[vid] raises IndexError.  The generic kernels (K1 -> K2 -> K3), the unfused
+    and the fused static warp kernels must report the first offending batch and neither gather nor tally out of
+    bounds."""
+    import torch
+    mesh = P.gen_grid(90, 90)
+    cfg = BatchConfig()
+    idx = mesh.indices.copy()
+    stat = strategy in ("naive", "warp")
+    offs = O.static_batches(len(idx)) if stat else O.dynamic_batches(idx)
+    bad_batch = 7
+    idx[offs[bad_batch] + 4] = mesh.vertex_count + 11
+    idx[offs[bad_batch + 9] + 1] = 0xFFFFFF00
+    if not stat:
+        offs = O.dynamic_batches(idx)
+        bad_batch = int(np.searchsorted(offs, np.flatnonzero(idx >= mesh.vertex_count)[0], side="right") - 1)
+    guard = torch.full((mesh.vertex_count + 4096,), 7, dtype=torch.int32, device="cuda")  # counts + canary behind them
+    variants = [dict()]
+    if strategy == "warp":
+        variants += [dict(static=True, fuse=False), dict(static=True)]
+    for kw in variants:
+        guard.fill_(7)
+        if shader == "position":
+            spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                                     matrix=MATRIX, vertex_count=mesh.vertex_count)
+        else:
+            spec = engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY, vertex_count=mesh.vertex_count)
+        o = torch.from_numpy(offs.astype(np.int32)).cuda()
+        bufs = engine.RunBuffers()
+        bufs.t["counts"] = guard[:mesh.vertex_count]  # the tally buffer, with the canary right behind it
+        run = engine.run_device(strategy, engine.to_device_indices(idx), o[:-1], o[1:], len(offs) - 1, len(idx),
+                                int(np.diff(offs).max()), cfg, HashConfig(), spec, want_counts=True, buffers=bufs, **kw)
+        with pytest.raises(IndexError, match=f"batch {bad_batch}\\)"):
+            run.check()
+        torch.cuda.synchronize()
+        assert int((guard[mesh.vertex_count:] != 7).sum()) == 0, "tally written out of bounds"
+    # through the public API
+    with pytest.raises(IndexError):
+        batches = P.offsets_to_batches(offs)
+        sh = P.position_shader(mesh, MATRIX) if shader == "position" else P.identity_shader()
+        P.run_on_indices(strategy, idx, batches, cfg, sh, HashConfig(), vertex_count=mesh.vertex_count)
+
+
+def test_equally_spaced_batches_off_quad_alignment(cuda_lib):
+    """[Batch(3,99), Batch(99,195)] looks like static_batches shifted by one primitive; the
+    position-aligned kernels need a 16-byte aligned start, so the list must take the general kernel instead of
+    failing with 'batch is not a primitive-aligned range'."""
+    mesh = P.gen_grid(30, 30)
+    cfg = BatchConfig()
+    for lists in ([Batch(3, 99), Batch(99, 195)], [Batch(3, 99)], [Batch(6, 102), Batch(102, 198), Batch(198, 240)],
+                  [Batch(12, 108), Batch(108, 204)], [Batch(0, 96), Batch(96, 150)]):
+        bb = np.array([b.begin for b in lists]), np.array([b.end for b in lists])
+        for strat in ("warp", "naive", "sort"):
+            out = P.run_on_indices(strat, mesh.indices, lists, cfg, P.identity_shader(), vertex_count=mesh.vertex_count)
+            fr = O.run(strat, mesh.indices, bb[0], bb[1])
+            assert_flat_equal(out[0].device_run.flat(), oracle_flat(fr), f"{strat} {lists}")
+            assert np.array_equal(out[0].as_array(), np.concatenate([mesh.indices[b.begin:b.end] for b in lists]))
+
+
+def test_stream_write_binary_roundtrip(cuda_lib, tmp_path):
+    """strategies.py:150-152 / cli.py:340-345 --dump-stream: flat native-endian dump of the per-corner records."""
+    mesh = P.shuffle_triangles(P.gen_grid(33, 21), 2)
+    cfg = BatchConfig()
+    dyn = P.dynamic_batches(mesh.indices, cfg)
+    stream, _ = P.run_sorting(mesh, dyn, cfg, P.position_shader(mesh, MATRIX))
+    path = tmp_path / "stream.bin"
+    stream.write_binary(path)
+    back = np.fromfile(path, dtype=np.float32).reshape(-1, 3)
+    assert back.shape == (len(mesh.indices), 3) and np.array_equal(back, stream.as_array())
+    pos = np.hstack([mesh.positions, np.ones((mesh.vertex_count, 1))]) @ MATRIX.T
+    want = (pos[:, :3] / pos[:, 3:4]).astype(np.float32)[mesh.indices]
+    np.testing.assert_allclose(back, want, rtol=1e-5, atol=1e-5)
+    ident, _ = P.run_sorting(mesh, dyn, cfg, P.identity_shader())
+    ident.write_binary(path)
+    assert np.array_equal(np.fromfile(path, dtype=np.uint32), mesh.indices)

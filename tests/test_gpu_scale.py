@@ -47,7 +47,20 @@ def test_config3_warp(cuda_lib, dragon_grid, path):
     if path == "fused":  # the persistent tile kernel: every output of the full run against the C oracle
         assert run.kernel_path == 3
         so = O.static_batches(len(mesh.indices))
-        assert_flat_equal(run.flat(), oracle_flat(O.run("warp", mesh.indices, so[:-1], so[1:])), "config 3, tile kernel")
+        fr = O.run("warp", mesh.indices, so[:-1], so[1:])
+        assert_flat_equal(run.flat(), oracle_flat(fr), "config 3, tile kernel")
+        # ... and with the position shader: all 8 100 190 shaded vertices against the float64 oracle shader
+        pspec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                                  matrix=MATRIX, vertex_count=mesh.vertex_count)
+        prun = engine.run_device("warp", d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 96, cfg, None, pspec,
+                                 want_counts=True, **kw).check()
+        assert prun.kernel_path == 3
+        pflat = prun.flat()
+        assert_flat_equal(pflat, oracle_flat(fr), "config 3, tile kernel, position shader")
+        want = O.shade_positions(mesh.positions, fr.unique_ids, MATRIX)
+        assert pflat["shaded"].shape[0] == 8100190
+        np.testing.assert_allclose(pflat["shaded"][:, :3], want, rtol=1e-5, atol=1e-5)
+        assert np.array_equal(pflat["shade_counts"], O.shade_counts(fr.unique_ids, mesh.vertex_count))
     # bit-exact against the oracle on a prefix and on a window in the middle of the stream
     for lo in (0, 3000 * 96 * 30):
         sub = mesh.indices[lo:lo + 96 * 3000 + 33]  # ragged last batch
@@ -95,6 +108,16 @@ def test_config3_mesh_dynamic_sort(cuda_lib, dragon_grid):
     assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
     h = offs.cpu().numpy().astype(np.int64)
     assert np.array_equal(h.astype(np.int64), O.dynamic_batches(mesh.indices))  # every boundary of the 21.6 M-index stream
+    # the complete flat output (28 350 batches) against the oracle, then the shaded positions
+    fr = O.run("sort", mesh.indices, h[:-1], h[1:])
+    assert_flat_equal(run.flat(), oracle_flat(fr), "config 3 mesh, dynamic sort, full")
+    pspec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                              matrix=MATRIX, vertex_count=mesh.vertex_count)
+    prun = engine.run_device("sort", d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 1023, cfg, None, pspec).check()
+    pflat = prun.flat()
+    assert_flat_equal(pflat, oracle_flat(fr), "config 3 mesh, dynamic sort, position shader")
+    np.testing.assert_allclose(pflat["shaded"][:, :3], O.shade_positions(mesh.positions, fr.unique_ids, MATRIX),
+                               rtol=1e-5, atol=1e-5)
 
 
 def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
@@ -110,6 +133,7 @@ def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
     assert h[0] == 0 and h[-1] == len(mesh.indices) and (np.diff(h) > 0).all() and (np.diff(h) % 3 == 0).all()
     assert np.array_equal(h, O.dynamic_batches(mesh.indices))  # every boundary
     k = 3000
+    pos4 = engine.to_device_positions4(mesh.positions)
     for strat in ("hash", "sort", "phash"):
         run = engine.run_device(strat, d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 1023, cfg,
                                 HashConfig(), engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY)).check()
@@ -117,6 +141,18 @@ def test_config4_shuffled_hash_and_sort(cuda_lib, dragon_grid):
         if strat == "hash":
             assert run.probes == (216377586, 0, 256)
         assert np.array_equal(run.expand_stream(False).cpu().numpy().view(np.uint32), mesh.indices)
+        # the COMPLETE flat output of all 84 672 batches and the probe statistics against the oracle
+        full = O.run(strat, mesh.indices, h[:-1], h[1:])
+        assert_flat_equal(run.flat(), oracle_flat(full), f"config4 {strat} full")
+        if strat in ("hash", "phash"):
+            assert run.probes == (full.probes_fast, full.probes_slow, full.probe_max_chain), strat
+        # position shader on the shuffled stream (random gathers), every shaded vertex
+        prun = engine.run_device(strat, d_idx, offs[:-1], offs[1:], nb, len(mesh.indices), 1023, cfg, HashConfig(),
+                                 engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=pos4, matrix=MATRIX,
+                                                   vertex_count=mesh.vertex_count)).check()
+        got = prun.shaded4[:prun.invocations, :3].cpu().numpy()
+        np.testing.assert_allclose(got, O.shade_positions(mesh.positions, full.unique_ids, MATRIX), rtol=1e-5, atol=1e-5)
+        del full, got, prun
         sub_offs = h[:k + 1]
         fr = O.run(strat, mesh.indices, sub_offs[:-1], sub_offs[1:])
         sub = engine.run_device(strat, d_idx, offs[:k], offs[1:k + 1], k, int(sub_offs[-1]), 1023, cfg,

@@ -112,7 +112,7 @@ def test_index_outside_vertex_buffer_is_an_error(cuda_lib):
     spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
                              matrix=MATRIX, vertex_count=mesh.vertex_count)
     run, _ = tile_run(idx, BatchConfig(), spec)
-    with pytest.raises(ConfigError, match="batch 70"):
+    with pytest.raises(IndexError, match="batch 70"):  # strategies.py:62-65 positions[vid]
         run.check()
 
 

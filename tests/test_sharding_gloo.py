@@ -41,6 +41,53 @@ def test_lpt_assign_balances():
     assert all((np.diff(p) > 0).all() for p in parts)
 
 
+def test_merge_stats_names_the_first_failing_batch_of_the_stream():
+    """rank-local error words carry shard-relative batch numbers; the merge adds the shard's first
+    batch before taking the minimum, sums the counters and takes the max of the chain length."""
+    blocks = torch.zeros((3, N.VR_STATS_WORDS), dtype=torch.int64)
+    blocks[:, N.VR_STAT_ERROR] = -1
+    blocks[:, N.VR_STAT_INVOCATIONS] = torch.tensor([5, 7, 11])
+    blocks[:, N.VR_STAT_PROBE_MAX_CHAIN] = torch.tensor([3, 9, 4])
+    blocks[:, shard.STAT_BATCH_BASE] = torch.tensor([0, 100, 200])
+    out = shard.merge_stats(blocks)
+    assert int(out[N.VR_STAT_INVOCATIONS]) == 23 and int(out[N.VR_STAT_PROBE_MAX_CHAIN]) == 9
+    assert int(out[N.VR_STAT_ERROR]) == -1
+    blocks[2, N.VR_STAT_ERROR] = (1 << 8) | N.VR_ERR_HASH_FULL       # stream batch 201
+    blocks[1, N.VR_STAT_ERROR] = (50 << 8) | N.VR_ERR_OVER_BUDGET    # stream batch 150: earlier in the stream
+    out = shard.merge_stats(blocks)
+    assert int(out[N.VR_STAT_ERROR]) == (150 << 8) | N.VR_ERR_OVER_BUDGET
+
+
+def test_concat_flats_is_the_ordered_merge():
+    """strategies.py:472-483: per-shard results concatenated in rank order == the unsharded result (oracle on
+    both sides: this checks the host-side merge and the shard plans, the GPU test checks the device runs)."""
+    import oracle as O
+    from helpers import assert_flat_equal, oracle_flat
+    _, idx = O.gen_grid(50, 37)
+    offs = O.dynamic_batches(idx, max_unique=32, max_indices=127)
+    whole = O.run("hash", idx, offs[:-1], offs[1:], max_unique=32, table_size=32)
+    for world in (1, 2, 3, 8, 500):
+        flats, nb = [], 0
+        for r in range(world):
+            plan = shard.plan_from_offsets(offs, r, world)
+            assert plan.batch_lo == nb and (plan.index_lo, plan.index_hi) == (offs[plan.batch_lo], offs[plan.batch_hi])
+            nb = plan.batch_hi
+            if plan.n_batches == 0:
+                flats.append(None)
+                continue
+            mine = offs[plan.batch_lo:plan.batch_hi + 1]
+            flats.append(oracle_flat(O.run("hash", idx, mine[:-1], mine[1:], max_unique=32, table_size=32)))
+        assert nb == len(offs) - 1
+        assert_flat_equal(shard.concat_flats(flats), oracle_flat(whole), f"world {world}")
+    so = O.static_batches(len(idx))
+    from paper_1805_08893_b200.batching import BatchConfig
+    for world in (2, 3, 7):
+        plans = [shard.plan_static(len(idx), BatchConfig(), r, world) for r in range(world)]
+        assert plans[0].index_lo == 0 and plans[-1].index_hi == len(idx)
+        assert all(a.index_hi == b.index_lo and a.batch_hi == b.batch_lo for a, b in zip(plans, plans[1:]))
+        assert all(p.index_lo == so[p.batch_lo] and p.index_hi == so[p.batch_hi] for p in plans)
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -64,7 +111,8 @@ def _worker(rank, world, port, q):
         stats[N.VR_STAT_ROUNDS] = fr.rounds
         stats[N.VR_STAT_PROBES_FAST] = fr.probes_fast
         stats[N.VR_STAT_PROBE_MAX_CHAIN] = fr.probe_max_chain
-    total = shard.reduce_stats(stats)
+    lo, _ = shard.shard_range(len(offs) - 1, rank, world)
+    total = shard.reduce_stats(stats, batch_base=lo)
     if rank == 0:
         q.put(total.tolist())
     dist.destroy_process_group()
