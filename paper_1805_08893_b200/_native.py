@@ -29,6 +29,11 @@ VR_SHADER_NONE, VR_SHADER_IDENTITY, VR_SHADER_POSITION = range(3)
 VR_STATS_WORDS = 16
 VR_PROFILE_STAGES = 4
 PROFILE_STAGE_NAMES = ("init", "dedup", "offset_scan", "shade_finalize")
+# vr_last_kernel_path() values that are ONE kernel for dedup + output offsets + shading
+KERNEL_PATH_NAMES = {
+    2: "fused static warp kernel (dedup + look-back + shade)",
+    3: "persistent tile kernel (stage + dedup + decoupled look-back/shade)",
+}
 
 
 class NativeLibraryError(RuntimeError):

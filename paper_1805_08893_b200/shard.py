@@ -64,34 +64,42 @@ def lpt_assign(sizes, world: int):
 # ---------------------------------------------------------------------------------------------
 # statistics: one collective
 # ---------------------------------------------------------------------------------------------
-def merge_stats(blocks: torch.Tensor) -> torch.Tensor:
-    """[world, VR_STATS_WORDS] per-rank blocks -> the block of the whole stream (strategies.py:472-483).
-    The error word of a rank holds (batch within its shard << 8 | status); word STAT_BATCH_BASE holds the
-    shard's first batch, so the merged word names the first failing batch of the STREAM."""
-    out = torch.zeros(N.VR_STATS_WORDS, dtype=torch.int64, device=blocks.device)
+def merge_stats(blocks) -> torch.Tensor:
+    """[world, VR_STATS_WORDS] per-rank blocks (tensor or array) -> the block of the whole stream, a CPU int64
+    tensor (strategies.py:472-483).  The error word of a rank holds (batch within its shard << 8 | status); word
+    STAT_BATCH_BASE holds the shard's first batch, so the merged word names the first failing batch of the STREAM."""
+    b = blocks.detach().cpu().numpy() if isinstance(blocks, torch.Tensor) else np.asarray(blocks)
+    b = b.reshape(-1, N.VR_STATS_WORDS).astype(np.int64)
+    out = np.zeros(N.VR_STATS_WORDS, dtype=np.int64)
     for w in SUM_WORDS:
-        out[w] = blocks[:, w].sum()
+        out[w] = b[:, w].sum()
     for w in MAX_WORDS:
-        out[w] = blocks[:, w].max()
-    err = blocks[:, N.VR_STAT_ERROR]
-    glob = (((err >> 8) + blocks[:, STAT_BATCH_BASE]) << 8) | (err & 0xFF)
-    big = torch.full_like(err, 2 ** 62)
-    first = torch.where(err < 0, big, glob).min()
-    out[N.VR_STAT_ERROR] = torch.where(first >= 2 ** 62, torch.full_like(first, -1), first)
+        out[w] = b[:, w].max()
+    err = b[:, N.VR_STAT_ERROR]
+    glob = (((err >> 8) + b[:, STAT_BATCH_BASE]) << 8) | (err & 0xFF)
+    bad = glob[err >= 0]
+    out[N.VR_STAT_ERROR] = bad.min() if len(bad) else -1
+    return torch.from_numpy(out)
+
+
+def gather_stats(stats: torch.Tensor, group=None, batch_base: int = 0) -> torch.Tensor:
+    """The ONE collective of a sharded run: all-gather of the ranks' statistics blocks -> [world, VR_STATS_WORDS]
+    on the device of `stats` (NCCL for CUDA tensors, gloo for CPU tensors); asynchronous on the current stream.
+    Merge with `merge_stats` when the host wants the numbers."""
+    s = stats.clone()
+    s[STAT_BATCH_BASE] = batch_base
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return s.unsqueeze(0)
+    world = dist.get_world_size(group)
+    out = torch.empty((world, s.numel()), dtype=s.dtype, device=s.device)
+    dist.all_gather(list(out.unbind(0)), s, group=group)
     return out
 
 
 def reduce_stats(stats: torch.Tensor, group=None, batch_base: int = 0) -> torch.Tensor:
-    """One statistics block per rank -> the block of the whole job, on every rank: ONE all-gather of
-    VR_STATS_WORDS int64 (NCCL for CUDA tensors, gloo for CPU tensors) and a local merge."""
-    s = stats.clone()
-    s[STAT_BATCH_BASE] = batch_base
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
-        return merge_stats(s.unsqueeze(0))
-    world = dist.get_world_size(group)
-    parts = [torch.empty_like(s) for _ in range(world)]
-    dist.all_gather(parts, s, group=group)
-    return merge_stats(torch.stack(parts))
+    """One statistics block per rank -> the block of the whole job on every rank (CPU tensor): one all-gather
+    of VR_STATS_WORDS int64 and a host-side merge."""
+    return merge_stats(gather_stats(stats, group, batch_base))
 
 
 # ---------------------------------------------------------------------------------------------

@@ -93,3 +93,89 @@ def test_stream_write_binary_roundtrip(cuda_lib, tmp_path):
     ident, _ = P.run_sorting(mesh, dyn, cfg, P.identity_shader())
     ident.write_binary(path)
     assert np.array_equal(np.fromfile(path, dtype=np.uint32), mesh.indices)
+
+
+@pytest.mark.parametrize("case", ["static-warp", "dynamic-hash", "dynamic-sort", "static-naive"])
+def test_sharded_runs_concatenate_to_the_unsharded_result(cuda_lib, case):
+    """SURVEY.md 8e / strategies.py:465-483: one stream cut into whole batches per rank.  The shards of world =
+    2, 3, 8 are run one after another on this GPU through shard.run_sharded (the code every rank runs); their
+    ordered merge must equal the single-GPU result byte for byte, statistics and per-vertex tallies included."""
+    from paper_1805_08893_b200 import shard
+    import torch
+    batching, strategy = case.split("-")
+    mesh = P.shuffle_triangles(P.gen_grid(150, 131), 9) if batching == "dynamic" else P.gen_grid(150, 131)
+    cfg = BatchConfig()
+    hc = HashConfig()
+    d_idx = engine.to_device_indices(mesh.indices)
+    spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                             matrix=MATRIX, vertex_count=mesh.vertex_count)
+    whole, plan1 = shard.run_sharded(strategy, d_idx, cfg, hc, spec, batching=batching, rank=0, world=1, want_counts=True)
+    want = whole.flat()
+    want_stats = whole.stats().copy()
+    if strategy == "warp":
+        assert whole.kernel_path == 3  # the persistent tile kernel
+    for world in (2, 3, 8):
+        flats, blocks, nb = [], [], 0
+        for rank in range(world):
+            run, plan = shard.run_sharded(strategy, d_idx, cfg, hc, spec, batching=batching, rank=rank, world=world,
+                                          want_counts=True)
+            assert plan.batch_lo == nb
+            nb = plan.batch_hi
+            flats.append(run.flat())
+            s = run.stats_dev.clone()
+            s[shard.STAT_BATCH_BASE] = plan.batch_lo
+            blocks.append(s)
+        assert nb == plan1.n_batches
+        got = shard.concat_flats(flats)
+        assert_flat_equal(got, want, f"{case} world {world}")
+        assert np.array_equal(got["shaded"], want["shaded"])  # same kernels, same arithmetic: bit-identical
+        assert np.array_equal(got["shade_counts"], want["shade_counts"])
+        total = shard.merge_stats(torch.stack(blocks)).cpu().numpy()
+        assert np.array_equal(total[:8], want_stats[:8]), (total, want_stats)
+
+
+def test_sharded_error_names_the_stream_batch(cuda_lib):
+    """The merged error word names the first failing batch of the STREAM, not of a shard."""
+    from paper_1805_08893_b200 import shard
+    import torch
+    mesh = P.gen_grid(60, 60)
+    idx = mesh.indices.copy()
+    idx[96 * 55 + 7] = mesh.vertex_count + 1  # stream batch 55
+    idx[96 * 40 + 7] = mesh.vertex_count + 2  # stream batch 40: the first one
+    d_idx = engine.to_device_indices(idx)
+    spec = engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY, vertex_count=mesh.vertex_count)
+    blocks = []
+    for rank in range(4):
+        run, plan = shard.run_sharded("warp", d_idx, BatchConfig(), None, spec, batching="static", rank=rank, world=4,
+                                      want_counts=True)
+        s = run.stats_dev.clone()
+        s[shard.STAT_BATCH_BASE] = plan.batch_lo
+        blocks.append(s)
+    err = int(shard.merge_stats(torch.stack(blocks))[N.VR_STAT_ERROR])
+    assert (err >> 8, err & 0xFF) == (40, N.VR_ERR_VERTEX_RANGE)
+
+
+def test_sharded_multidraw_scene(cuda_lib):
+    """configs[4] across ranks: whole draws per rank (LPT); the per-draw reports of all ranks together equal the
+    per-draw reports of the single-GPU packed run."""
+    from paper_1805_08893_b200 import draws as D
+    from paper_1805_08893_b200 import shard
+    meshes = D.scene_corpus(24, seed=5, lo=10, hi=40, ico=(1, 3))
+    cfg = BatchConfig()
+    ds = D.pack_draws(meshes)
+    offs = D.dynamic_offsets_draws(ds, cfg)
+    whole = D.run_draws("hash", ds, offs, cfg, HashConfig(), matrix=MATRIX)
+    want = [(r.indices, r.invocations, r.batches) for r in D.per_draw_reports(whole, ds, offs, "hash")]
+    for world in (2, 5):
+        got = {}
+        tot = np.zeros(8, dtype=np.int64)
+        for rank in range(world):
+            run, rds, roffs, mine = shard.run_draws_sharded("hash", meshes, cfg, HashConfig(), rank=rank, world=world,
+                                                           matrix=MATRIX)
+            for d, r in zip(mine, D.per_draw_reports(run, rds, roffs, "hash")):
+                got[int(d)] = (r.indices, r.invocations, r.batches)
+            st = run.stats()
+            tot[:6] += st[:6]
+            tot[6] = max(tot[6], st[6])
+        assert [got[d] for d in range(len(meshes))] == want
+        assert np.array_equal(tot[:7], whole.stats()[:7])
