@@ -13,11 +13,13 @@
 //                    offsets and the vertex shader once per unique id
 //                    (strategies.py:456-463), 16-byte gathers / coalesced 16-byte stores,
 //                    optional attribute pass-through and per-vertex tally (:485-489)
+#include <type_traits>
+
 #include "vr_common.cuh"
 
 namespace vr {
 
-enum { ACC_PROBES_FAST = 0, ACC_PROBES_SLOW, ACC_MAX_CHAIN, ACC_ERROR, ACC_ABORT, ACC_TICKET, ACC_WORDS = 8 };
+enum { ACC_PROBES_FAST = 0, ACC_PROBES_SLOW, ACC_MAX_CHAIN, ACC_ERROR, ACC_ABORT, ACC_TICKET, ACC_DONE, ACC_WORDS = 8 };
 
 struct RunCtx {
     const uint32_t* __restrict__ idx;
@@ -368,10 +370,11 @@ __device__ void finish_stats(const RunCtx& c, long long R, long long U) {
     st[VR_STAT_INVOCATIONS] = U;
     st[VR_STAT_BATCHES] = c.n_batches;
     st[VR_STAT_ROUNDS] = R;
-    st[VR_STAT_PROBES_FAST] = c.acc[ACC_PROBES_FAST];
-    st[VR_STAT_PROBES_SLOW] = c.acc[ACC_PROBES_SLOW];
-    st[VR_STAT_PROBE_MAX_CHAIN] = c.acc[ACC_MAX_CHAIN];
-    const long long e = c.acc[ACC_ERROR];
+    // (read from L2: a fused kernel calls this from its last CTA, whose L1 may hold an older copy of the line)
+    st[VR_STAT_PROBES_FAST] = __ldcg(c.acc + ACC_PROBES_FAST);
+    st[VR_STAT_PROBES_SLOW] = __ldcg(c.acc + ACC_PROBES_SLOW);
+    st[VR_STAT_PROBE_MAX_CHAIN] = __ldcg(c.acc + ACC_MAX_CHAIN);
+    const long long e = __ldcg(c.acc + ACC_ERROR);
     if (e == 0) {
         if (c.out.d_batch_round_off) c.out.d_batch_round_off[c.n_batches] = (int32_t)R;
         if (c.out.d_round_uid_off) c.out.d_round_uid_off[R] = (int32_t)U;
@@ -1588,6 +1591,8 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
     }
 }
 
+#include "vr_dyn3.cuh"
+
 // ---------------------------------------------------------------------------------
 // strategies.py:456-463 expanded per-corner stream (the paper's stage output queue).
 // ---------------------------------------------------------------------------------
@@ -1667,7 +1672,7 @@ __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct WsLayout {
-    size_t map_off, counts, seg_counts, seg_off, tile_sums, tile_off, acc, tile_state, stage_uid, stage_round, total;
+    size_t map_off, counts, seg_counts, seg_off, tile_sums, tile_off, acc, tile_state, stage_uid, stage_round, aux, total;
     int stage_factor, seg_batches, n_segs, n_scan_tiles;
 };
 
@@ -1689,7 +1694,8 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.tile_off = o; o += align_up((size_t)(L.n_scan_tiles + 2) * 8);
     L.acc = o; o += align_up(ACC_WORDS * 8);
     // kRowThreads tiles (>= kFastThreads tiles) + the tile kernel's two group tables (one group = 32 tiles)
-    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 64) + 1 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);
+    // (and the kDyn3Warps-batch tiles of the three-kernel sort/hash path)
+    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 8) + 1 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);
     L.stage_uid = o;
     if (strategy != VR_NAIVE) {
         size_t words = (size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64;
@@ -1701,6 +1707,8 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     }
     L.stage_round = o;
     if (strategy == VR_WARP) o += align_up(((size_t)span_total / ps + nb + 64) * 4);
+    L.aux = o;  // vr_dyn3.cuh: home slot / table slot / group of every distinct id
+    if (strategy == VR_HASH || strategy == VR_PHASH) o += align_up((size_t)span_total * 4 + (size_t)nb * 128 + 256);
     L.total = o;
     return L;
 }
@@ -1955,9 +1963,13 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     const bool rows = fused && rows_geometry(cfg->warp_width, cfg->batch_size, rg) &&
                       (((uintptr_t)out->d_assembly_map) & 15) == 0 && shader && shader->vertex_count > 0 &&
                       shader->vertex_count <= (1 << 24);
-    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : 0;
+    // budgeted sort / hash / phash batches: the three-kernel path of vr_dyn3.cuh
+    Dyn3Plan d3 = dyn3_plan(strategy, cfg, hc, max_span, c.enforce_budget != 0, shader, out);
+    if (!allow_fuse || nb == 0 || nb >= (1 << 30)) d3.ok = false;
+    d3.g.aux = ws + L.aux;
+    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, kDyn3Warps) : 0;
     g_prof_marks = 0;
-    g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : 0;
+    g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : d3.ok ? 4 : 0;
     prof_mark(stream);
     c.n_state_words = rows ? c.n_fused_tiles + 1 + 2 * ((int)ceil_div(c.n_fused_tiles, kRowGroup) + 1) : c.n_fused_tiles;
     init_kernel<<<(int)ceil_div(c.n_state_words + ACC_WORDS, 256), 256, 0, stream>>>(c);
@@ -1966,6 +1978,31 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (nb > 0) {
         if (strategy == VR_NAIVE) {
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
+        } else if (d3.ok) {
+            const int tiles = c.n_fused_tiles;
+            if (strategy == VR_SORT) {
+                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
+                dyn3_dedup_kernel<false, false><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
+            } else if (strategy == VR_HASH) {
+                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
+                dyn3_dedup_kernel<true, false><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
+                dyn3_insert_kernel<false><<<(int)ceil_div(nb, kDyn3InsertThreads), kDyn3InsertThreads, 0, stream>>>(c, d3.g);
+            } else {
+                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
+                dyn3_dedup_kernel<true, true><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
+                dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads), kDyn3InsertThreads, 0, stream>>>(c, d3.g);
+            }
+            prof_mark(stream);
+            prof_mark(stream);
+            switch (strategy) {
+            case VR_SORT: dyn3_finish_kernel<VR_SORT><<<tiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            case VR_HASH: dyn3_finish_kernel<VR_HASH><<<tiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            default: dyn3_finish_kernel<VR_PHASH><<<tiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            }
+            prof_mark(stream);
+            g_last_launches = strategy == VR_SORT ? 3 : 4;
+            VR_CUDA_CHECK(cudaGetLastError());
+            return VR_OK;
         } else if (rows) {
             const int bs = cfg->batch_size;
             switch (cfg->warp_width) {
