@@ -37,6 +37,35 @@ __host__ __device__ inline int ilog2(uint32_t pow2) {
 #endif
 }
 
+// Ablation / debugging knobs.  Read from the environment ONCE per process (the first library call that
+// asks); the launch paths never call getenv.  Defaults are the product behaviour.
+struct DebugKnobs {
+    int link_tile = 2048;     // VR_LINK_TILE     batch formation: positions per tile of the link kernel
+    int links_warp = 0;       // VR_LINKS_WARP    batch formation: per-warp link kernel instead of the tile kernel
+    int greedy_run = 64;      // VR_GREEDY_RUN
+    int greedy_global = 0;    // VR_GREEDY_GLOBAL batch formation: windows walked in global memory
+    int walk_global = 0;      // VR_WALK_GLOBAL   batch formation: chain walks in global memory
+    int sort_cta = 0;         // VR_SORT_CTA      general sort path: one CTA per batch
+    int rows_prefetch = 0;    // VR_PREFETCH      tile kernel: L2 prefetch of a tile's vertices
+    int rows_lag = 0;         // VR_LAG           tile kernel: shade lag in tiles (0 = 1.5 x resident CTAs)
+    int no_pdl = 0;           // VR_NO_PDL        no programmatic dependent launch
+    int dyn3_prefetch = 0;    // VR_DYN3_PREFETCH three-kernel path: L2 prefetch of the distinct vertices before the sort
+    int dyn_single = 0;       // VR_DYN_SINGLE    batch formation: (reserved)
+};
+inline const DebugKnobs& debug_knobs() {
+    static const DebugKnobs k = [] {
+        DebugKnobs d;
+        auto geti = [](const char* name, int& v) { if (const char* e = getenv(name)) v = atoi(e); };
+        auto flag = [](const char* name, int& v) { if (getenv(name)) v = 1; };
+        geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run);
+        flag("VR_GREEDY_GLOBAL", d.greedy_global); flag("VR_WALK_GLOBAL", d.walk_global); flag("VR_SORT_CTA", d.sort_cta);
+        geti("VR_PREFETCH", d.rows_prefetch); geti("VR_LAG", d.rows_lag); flag("VR_NO_PDL", d.no_pdl);
+        geti("VR_DYN3_PREFETCH", d.dyn3_prefetch); geti("VR_DYN_SINGLE", d.dyn_single);
+        return d;
+    }();
+    return k;
+}
+
 // strategies.py:88-91 HashConfig.slot; bits == 0 (table_size 1) -> slot 0.
 __device__ __forceinline__ uint32_t hash_slot(uint32_t vid, uint32_t mult, int bits) {
     uint32_t prod = vid * mult;
@@ -93,6 +122,28 @@ struct ShaderParams {
     int vertex_count;
     const int32_t* __restrict__ batch_base;  // multi-draw: first vertex of each batch's draw, or NULL
 };
+
+// L2 eviction policies (createpolicy + .L2::cache_hint): a random 16-byte gather pulls a 32-byte sector, so a
+// vertex buffer that has to come from DRAM costs twice its algorithmic bytes per invocation; kept in L2 (it is
+// 58 MB at 3.6 M vertices) it costs them once per run.  The outputs are written once and never read here.
+struct L2Policies { unsigned long long keep, stream; };
+__device__ __forceinline__ L2Policies make_l2_policies() {
+    L2Policies p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p.keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p.stream));
+    return p;
+}
+__device__ __forceinline__ float4 ldg_keep_f4(const float4* p, unsigned long long pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_stream_f4(float4* p, float4 v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v, unsigned long long pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
 
 // The w-divide uses one hardware reciprocal (MUFU.RCP, <= 1 ulp) and three multiplies: a few ulp
 // of FP32 from the reference's float64 result, far inside the 1e-5 relative bound.

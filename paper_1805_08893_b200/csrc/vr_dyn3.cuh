@@ -27,8 +27,9 @@
 // batch and table_size <= 256 (d, slots and ranks are bytes), ids < 2^24 for sort (packed sort key).
 #pragma once
 
-constexpr int kDyn3Warps = 8;          // batches per CTA of kernels A and C
-constexpr int kDyn3InsertThreads = 128;
+constexpr int kDyn3Warps = 8;          // warps per CTA of kernels A and C
+constexpr int kDyn3Tile = 32;          // batches per CTA of kernel A (one look-back per tile)
+constexpr int kDyn3InsertThreads = 128;  // batches per CTA of kernel B (hash); phash keeps more per batch: half of that
 
 struct Dyn3Geom {
     int q;               // slots of the private set (power of two)
@@ -37,52 +38,62 @@ struct Dyn3Geom {
     int per_warp_bytes;  // shared memory per warp of kernel A
     int w, mfp;          // phash: group width, fast probes
     int strategy;
-    unsigned char* aux;  // hash/phash: per batch home[span'] | slot[span'] | grp u16[span']
+    int prefetch;        // kernel C: L2 prefetch of the distinct vertices before they are put in order
+    unsigned char* aux;  // hash/phash: per batch occupancy bitmap[32 B] | home[span'] | slot[span'] | grp u16[span']
 };
 
 __device__ __forceinline__ int64_t dyn3_aux_base(const RunCtx& c, int b, int mo) { return ((int64_t)mo * 4 + (int64_t)b * 128) & ~15LL; }
 __device__ __forceinline__ int dyn3_aux_stride(int span) { return (span + 15) & ~15; }
+constexpr int kDyn3AuxHome = 32;  // byte offset of home[] behind the bitmap
 
 // ---- A ------------------------------------------------------------------------------------------
 template <bool ORDERED, bool PHASH>
 __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, Dyn3Geom g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_tile;
-    __shared__ int2 s_cnt[kDyn3Warps];
+    __shared__ int2 s_cnt[kDyn3Tile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long*)&c.acc[ACC_TICKET], 1ull);  // tiles in ticket order
     __syncthreads();
     const int tile = s_tile;
-    const int b = tile * kDyn3Warps + wid;
-    int rounds = 0, nu = 0;
-    if (b < c.n_batches && !c.acc[ACC_ABORT]) {
-        unsigned char* base = smem_raw + (size_t)wid * g.per_warp_bytes;
-        uint32_t* kkey = reinterpret_cast<uint32_t*>(base);           // [q] the set
-        uint32_t* kpos = kkey + g.q;                                  // [q] smallest position of the id (ORDERED)
-        uint16_t* kidx = reinterpret_cast<uint16_t*>(ORDERED ? kpos + g.q : kpos);  // [q] number d of the id
+    const bool abort = c.acc[ACC_ABORT] != 0;
+    unsigned char* base = smem_raw + (size_t)wid * g.per_warp_bytes;
+    uint32_t* kkey = reinterpret_cast<uint32_t*>(base);  // [q] the set
+    // ORDERED: [q] smallest position of the id while its first step is open, its number d afterwards (d <= every
+    // position of the id, so later atomicMin's leave it alone); else u16 [q] number d of the id
+    uint32_t* kpos = kkey + g.q;
+    uint16_t* kidx = reinterpret_cast<uint16_t*>(kpos);
+    const uint32_t qmask = (uint32_t)g.q - 1;
+    const int qshift = 32 - ilog2((uint32_t)g.q);
+    const uint32_t lt = (1u << lane) - 1;
+    const int wshift = PHASH ? ilog2((uint32_t)g.w) : 0;
+#pragma unroll 1
+    for (int k = 0; k < kDyn3Tile / kDyn3Warps; k++) {
+        const int slot_in_tile = k * kDyn3Warps + wid;
+        const int b = tile * kDyn3Tile + slot_in_tile;
+        int rounds = 0, nu = 0;
         int begin, n;
-        if (validate_batch(c, b, begin, n)) {
+        if (b < c.n_batches && !abort && validate_batch(c, b, begin, n)) {
             const int mo = batch_map_off(c, b, begin);
-            const uint32_t qmask = (uint32_t)g.q - 1;
-            const int qshift = 32 - ilog2((uint32_t)g.q);
             const uint32_t* __restrict__ ids = c.idx + begin;
             uint16_t* __restrict__ dmap = c.out.d_assembly_map + mo;
             uint32_t* __restrict__ dist = c.stage_uid + stage_uid_base(c, b, mo);
             unsigned char* __restrict__ home = nullptr;
             uint16_t* __restrict__ grp = nullptr;
             if (ORDERED) {
-                home = g.aux + dyn3_aux_base(c, b, mo);
+                home = g.aux + dyn3_aux_base(c, b, mo) + kDyn3AuxHome;
                 grp = reinterpret_cast<uint16_t*>(home + 2 * dyn3_aux_stride(n));
             }
+            uint32_t id_next = lane < n ? __ldg(ids + lane) : 0u;
+            __syncwarp();
             for (int i = 4 * lane; i < g.q; i += 128) {
                 *reinterpret_cast<uint4*>(kkey + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
                 if (ORDERED) *reinterpret_cast<uint4*>(kpos + i) = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
             }
             __syncwarp();
-            const uint32_t lt = (1u << lane) - 1;
-            const int wshift = PHASH ? ilog2((uint32_t)g.w) : 0;
             bool overflow = false;
-            uint32_t id_next = lane < n ? __ldg(ids + lane) : 0u;
+            // (two elements per lane and step with interleaved probe chains: measured slower on the short batches of
+            // a shuffled mesh -- 40+ registers instead of 32 cost more warps than the shared ballots saved)
             for (int i0 = 0; i0 < n; i0 += 32) {
                 const int i = i0 + lane;
                 const bool valid = i < n;
@@ -101,7 +112,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                 }
                 if (ORDERED) {
                     // the reference inserts in batch order: among equal ids of this step the lowest position is the
-                    // first occurrence (earlier steps hold smaller positions already)
+                    // first occurrence (ids of earlier steps hold their d, which is below every later position)
                     __syncwarp();
                     first = valid && kpos[h] == (uint32_t)i;
                 }
@@ -110,13 +121,13 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                 nu += __popc(m);
                 if (nu > g.u_bound) { overflow = true; break; }  // uniform
                 if (first) {
-                    kidx[h] = (uint16_t)d;
+                    if (ORDERED) kpos[h] = (uint32_t)d; else kidx[h] = (uint16_t)d;
                     dist[d] = id;
                     if (ORDERED) home[d] = (unsigned char)hash_slot(id, c.multiplier, c.table_bits);
                     if (PHASH) grp[d] = (uint16_t)(i >> wshift);
                 }
                 __syncwarp();
-                if (valid) dmap[i] = kidx[h];
+                if (valid) dmap[i] = ORDERED ? (uint16_t)kpos[h] : kidx[h];
             }
             rounds = 1;
             if (overflow) {  // strategies.py:451-455 / :283-284
@@ -127,16 +138,16 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                 if (lane == 0) report_error(c, b, VR_ERR_OVER_BUDGET);
             }
         }
-    }
-    if (lane == 0) {
-        s_cnt[wid] = make_int2(rounds, nu);
-        if (b < c.n_batches) c.counts[b] = make_int2(rounds, nu);
+        if (lane == 0) {
+            s_cnt[slot_in_tile] = make_int2(rounds, nu);
+            if (b < c.n_batches) c.counts[b] = make_int2(rounds, nu);
+        }
     }
     __syncthreads();
     // ---- output offsets: decoupled look-back over tiles (every predecessor holds an earlier ticket, so it is
     // resident or finished)
     if (wid == 0) {
-        const int2 v = lane < kDyn3Warps ? s_cnt[lane] : make_int2(0, 0);
+        const int2 v = s_cnt[lane];
         const int ir = warp_incl_scan(v.x, lane), iu = warp_incl_scan(v.y, lane);
         const long long ar = __shfl_sync(0xffffffffu, ir, 31), au = __shfl_sync(0xffffffffu, iu, 31);
         unsigned long long* __restrict__ state = c.tile_state;
@@ -152,8 +163,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                 for (;;) {
                     if (idx >= 0) word = ld_relaxed_gpu_u64(state + idx);
                     if (__all_sync(0xffffffffu, (word >> 62) != 0)) break;
-                    if (++spins > (1 << 12)) __nanosleep(100);
-                    if (spins > (1 << 22)) { lost = true; break; }
+                    __nanosleep(64);  // the predecessors are busy deduplicating: leave them the issue slots
+                    if (++spins > (1 << 22)) { lost = true; break; }
                 }
                 if (lost) break;
                 const uint32_t incl = __ballot_sync(0xffffffffu, (word >> 62) == 2);
@@ -170,55 +181,68 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                 eu += __shfl_xor_sync(0xffffffffu, eu, d);
             }
             if (lane == 0) {
-                if (lost) report_error(c, (int64_t)tile * kDyn3Warps, VR_ERR_CUDA);
+                if (lost) report_error(c, (int64_t)tile * kDyn3Tile, VR_ERR_CUDA);
                 st_relaxed_gpu_u64(state + tile, kStateInclusive | ((unsigned long long)((er + ar) & 0x3FFFFFFF) << 32) | (unsigned long long)((eu + au) & 0xFFFFFFFFll));
             }
         }
-        const int bl = tile * kDyn3Warps + lane;
-        if (lane < kDyn3Warps && bl < c.n_batches)
+        const int bl = tile * kDyn3Tile + lane;
+        if (bl < c.n_batches)
             c.seg_off[bl] = make_int2((int)min(er + ir - v.x, 0x7fffffffLL), (int)min(eu + iu - v.y, 0x7fffffffLL));
-        if (lane == 0 && (tile + 1) * kDyn3Warps >= c.n_batches)
+        if (lane == 0 && (tile + 1) * kDyn3Tile >= c.n_batches)
             c.seg_off[c.n_batches] = make_int2((int)min(er + ar, 0x7fffffffLL), (int)min(eu + au, 0x7fffffffLL));
     }
 }
 
 // ---- B ------------------------------------------------------------------------------------------
-// Occupancy bitmap of one batch's table: words [w][thread] in shared memory (bank == lane).
+// Occupancy bitmap of one batch's table: words [w][thread] in shared memory (bank == lane); which words are
+// full is kept in a register, so a probe reads at most two words however full the table is.
+template <int NT>
 struct Dyn3Bitmap {
-    uint32_t* bm;  // + w * kDyn3InsertThreads
-    uint32_t wmask;
+    uint32_t* bm;  // + w * NT
+    uint32_t all;  // one bit per word
+    uint32_t full;
     __device__ __forceinline__ uint32_t next_free(uint32_t h) const {  // first free slot at or after h, circular
         uint32_t w = h >> 5;
-        uint32_t bits = ~bm[w * kDyn3InsertThreads] & (0xFFFFFFFFu << (h & 31));
-        while (bits == 0) {
-            w = (w + 1) & wmask;
-            bits = ~bm[w * kDyn3InsertThreads];
+        uint32_t bits = ~bm[w * NT] & (0xFFFFFFFFu << (h & 31));
+        if (bits == 0) {  // next word with a free slot, circular (w itself again last: its slots below h)
+            const uint32_t open = ~full & all;
+            const uint32_t above = open & ~((2u << w) - 1u);
+            w = (uint32_t)__ffs((int)(above ? above : open)) - 1;
+            bits = ~bm[w * NT];
         }
         return (w << 5) + (uint32_t)__ffs((int)bits) - 1;
     }
-    __device__ __forceinline__ void take(uint32_t s) { bm[(s >> 5) * kDyn3InsertThreads] |= 1u << (s & 31); }
+    __device__ __forceinline__ void take(uint32_t s) {
+        const uint32_t w = s >> 5;
+        const uint32_t v = bm[w * NT] | (1u << (s & 31));
+        bm[w * NT] = v;
+        if (v == 0xFFFFFFFFu) full |= 1u << w;
+    }
 };
 
 template <bool PHASH>
-__global__ void __launch_bounds__(kDyn3InsertThreads) dyn3_insert_kernel(RunCtx c, Dyn3Geom g) {
-    __shared__ uint32_t s_bm[8 * kDyn3InsertThreads];
-    __shared__ unsigned char s_dd[PHASH ? 64 * kDyn3InsertThreads : 1];  // deferred ids of the open group (d)
-    __shared__ unsigned char s_dh[PHASH ? 64 * kDyn3InsertThreads : 1];  //   and their home slots
+__global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertThreads) dyn3_insert_kernel(RunCtx c, Dyn3Geom g) {
+    constexpr int NT = PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertThreads;
+    __shared__ uint32_t s_bm[8 * NT];
+    __shared__ unsigned char s_dd[PHASH ? 64 * NT : 1];  // deferred ids of the open group (d)
+    __shared__ unsigned char s_dh[PHASH ? 64 * NT : 1];  //   and their home slots
+    __shared__ unsigned char s_slot[PHASH ? 256 * NT : 1];  // slot of every d (written out of order)
     const int t = threadIdx.x;
-    const int b = blockIdx.x * kDyn3InsertThreads + t;
+    const int b = blockIdx.x * NT + t;
     if (b >= c.n_batches) return;
     const int2 cnt = c.counts[b];
     if (cnt.x == 0 || cnt.y == 0) return;
     const int nu = cnt.y;
     const uint32_t tsize = c.table_size, tmask = tsize - 1;
     const int n_words = tsize >= 32 ? (int)(tsize >> 5) : 1;
-    Dyn3Bitmap B{s_bm + t, (uint32_t)n_words - 1};
-    for (int w = 0; w < n_words; w++) s_bm[w * kDyn3InsertThreads + t] = tsize >= 32 ? 0u : ~((1u << tsize) - 1u);
+    Dyn3Bitmap<NT> B{s_bm + t, (1u << n_words) - 1u, 0u};
+    for (int w = 0; w < n_words; w++) s_bm[w * NT + t] = tsize >= 32 ? 0u : ~((1u << tsize) - 1u);
     const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
     const int mo = batch_map_off(c, b, begin);
     const int stride = dyn3_aux_stride(n);
-    const unsigned char* __restrict__ home = g.aux + dyn3_aux_base(c, b, mo);
-    unsigned char* __restrict__ slot = g.aux + dyn3_aux_base(c, b, mo) + stride;
+    unsigned char* __restrict__ aux = g.aux + dyn3_aux_base(c, b, mo);
+    const unsigned char* __restrict__ home = aux + kDyn3AuxHome;
+    unsigned char* __restrict__ slot = aux + kDyn3AuxHome + stride;
     const uint16_t* __restrict__ grp = reinterpret_cast<const uint16_t*>(home + 2 * stride);
     if (!PHASH) {
         // strategies.py:277-294 on the distinct ids: next free slot at or after the home slot
@@ -245,37 +269,101 @@ __global__ void __launch_bounds__(kDyn3InsertThreads) dyn3_insert_kernel(RunCtx 
         int nd = 0, open_grp = -1;
         auto flush = [&]() {  // :345: the deferred ids one at a time, from where fast probing stopped
             for (int k = 0; k < nd; k++) {
-                const uint32_t d = s_dd[k * kDyn3InsertThreads + t], h = s_dh[k * kDyn3InsertThreads + t];
+                const uint32_t d = s_dd[k * NT + t], h = s_dh[k * NT + t];
                 const uint32_t s = B.next_free((h + mfp) & tmask);
                 B.take(s);
-                slot[d] = (unsigned char)s;
+                s_slot[d * NT + t] = (unsigned char)s;
             }
             nd = 0;
         };
-        for (int d = 0; d < nu; d++) {
-            const int gd = grp[d];
-            if (gd != open_grp) { flush(); open_grp = gd; }
-            const uint32_t h = home[d];
-            const uint32_t s = B.next_free(h);
-            if (((s - h) & tmask) < mfp) {  // :328-339 resolved by the fast pass
-                B.take(s);
-                slot[d] = (unsigned char)s;
-            } else {
-                s_dd[nd * kDyn3InsertThreads + t] = (unsigned char)d;
-                s_dh[nd * kDyn3InsertThreads + t] = (unsigned char)h;
-                nd++;
+        uint4 hv = *reinterpret_cast<const uint4*>(home);
+        uint4 g0 = *reinterpret_cast<const uint4*>(grp), g1 = *reinterpret_cast<const uint4*>(grp + 8);
+        for (int d0 = 0; d0 < nu; d0 += 16) {
+            const uint4 cur = hv, cg0 = g0, cg1 = g1;
+            if (d0 + 16 < nu) {
+                hv = *reinterpret_cast<const uint4*>(home + d0 + 16);
+                g0 = *reinterpret_cast<const uint4*>(grp + d0 + 16);
+                g1 = *reinterpret_cast<const uint4*>(grp + d0 + 24);
+            }
+            const uint32_t hw[4] = {cur.x, cur.y, cur.z, cur.w};
+            const uint32_t gw[8] = {cg0.x, cg0.y, cg0.z, cg0.w, cg1.x, cg1.y, cg1.z, cg1.w};
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+                const int d = d0 + k;
+                if (d < nu) {
+                    const int gd = (int)((gw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+                    if (gd != open_grp) { flush(); open_grp = gd; }
+                    const uint32_t h = (hw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
+                    const uint32_t s = B.next_free(h);
+                    if (((s - h) & tmask) < mfp) {  // :328-339 resolved by the fast pass
+                        B.take(s);
+                        s_slot[d * NT + t] = (unsigned char)s;
+                    } else {
+                        s_dd[nd * NT + t] = (unsigned char)d;
+                        s_dh[nd * NT + t] = (unsigned char)h;
+                        nd++;
+                    }
+                }
             }
         }
         flush();
+        for (int d0 = 0; d0 < nu; d0 += 16) {
+            uint32_t ow[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int k = 0; k < 16; k++) ow[k >> 2] |= (uint32_t)s_slot[(d0 + k) * NT + t] << (8 * (k & 3));
+            *reinterpret_cast<uint4*>(slot + d0) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        }
     }
+    // the table's occupancy for kernel C (ranks in table order, strategies.py:370-380)
+    uint32_t bw[8];
+#pragma unroll
+    for (int w = 0; w < 8; w++) bw[w] = w < n_words ? s_bm[w * NT + t] : 0u;
+    if (tsize < 32) bw[0] &= (1u << tsize) - 1u;
+    *reinterpret_cast<uint4*>(aux) = make_uint4(bw[0], bw[1], bw[2], bw[3]);
+    *reinterpret_cast<uint4*>(aux + 16) = make_uint4(bw[4], bw[5], bw[6], bw[7]);
 }
 
 // ---- C ------------------------------------------------------------------------------------------
+// Bitonic sort of 32 * R keys held R per lane, key index = lane * R + r ("blocked": the 3 innermost steps of
+// every merge stay inside a thread), every comparator ascending: a merge of size k first pairs i with
+// i ^ (k - 1), then i with i ^ j for j = k/4 .. 1, the lower index keeps the smaller key.
+template <int R>
+__device__ __forceinline__ void warp_bitonic_blocked(uint32_t (&v)[R], int lane) {
+#pragma unroll
+    for (int k = 2; k <= 32 * R; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            const int mask = (j == (k >> 1)) ? k - 1 : j;  // partner = i ^ mask
+            const int lmask = mask / R, rmask = mask % R;
+            if (lmask == 0) {
+#pragma unroll
+                for (int r = 0; r < R; r++) {
+                    if ((r ^ rmask) > r) {
+                        const uint32_t a = v[r], d = v[r ^ rmask];
+                        v[r] = min(a, d);
+                        v[r ^ rmask] = max(a, d);
+                    }
+                }
+            } else {
+                int top = lmask;  // highest set bit of the lane part decides who is the lower index
+                top |= top >> 1; top |= top >> 2; top |= top >> 4;
+                top = (top + 1) >> 1;
+                const bool lower = (lane & top) == 0;
+                uint32_t o[R];
+#pragma unroll
+                for (int r = 0; r < R; r++) o[r] = __shfl_xor_sync(0xffffffffu, v[r ^ rmask], lmask);
+#pragma unroll
+                for (int r = 0; r < R; r++) v[r] = lower ? min(v[r], o[r]) : max(v[r], o[r]);
+            }
+        }
+    }
+}
+
 template <int STRATEGY>
-__global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_finish_kernel(RunCtx c, ShaderParams sp, Dyn3Geom g) {
-    __shared__ uint32_t s_list[kDyn3Warps][256];   // the round's unique ids, in output order
-    __shared__ uint16_t s_of_d[kDyn3Warps][256];   // per distinct id d: distance home -> slot << 8 | position in the list
-    __shared__ uint32_t s_bm[kDyn3Warps][16];      // hash: occupancy words, then their exclusive popcount prefix
+__global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx c, ShaderParams sp, Dyn3Geom g) {
+    __shared__ __align__(16) uint32_t s_list[kDyn3Warps][256];  // the round's unique ids, in output order
+    __shared__ __align__(16) uint16_t s_of_d[kDyn3Warps][256];  // per distinct id d: distance home -> slot << 8 | position in the list
+    __shared__ uint32_t s_bm[kDyn3Warps][16];                   // hash: occupancy words, their exclusive popcount prefix
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int b = blockIdx.x * kDyn3Warps + wid;
     if (b < c.n_batches && !c.acc[ACC_ABORT]) {
@@ -290,76 +378,118 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_finish_kernel(RunCtx c, 
             uint32_t* list = s_list[wid];
             uint16_t* of_d = s_of_d[wid];
             const uint32_t* __restrict__ dist = c.stage_uid + stage_uid_base(c, b, mo);
+            const int vbase = sp.batch_base ? __ldg(sp.batch_base + b) : 0;
+            const bool want_pos = sp.kind == VR_SHADER_POSITION;
             if (lane == 0) {
                 if (c.out.d_round_uid_off) c.out.d_round_uid_off[off.x] = off.y;
                 if (c.out.d_round_prims) c.out.d_round_prims[off.x] = n / c.ps;
             }
-            if (STRATEGY == VR_SORT) {
-                // ascending ids: sort id << 8 | d in registers; position j holds the j-th smallest id and says which d it was
-                auto run = [&](auto rtag) {
-                    constexpr int R = decltype(rtag)::value;
-                    uint32_t v[R];
+            // the first 256 elements' numbers d are loaded before the list is put in order (their latency hides there)
+            uint16_t* __restrict__ amap = c.out.d_assembly_map + mo;
+            constexpr int EA = 8;
+            uint32_t early[EA];
 #pragma unroll
-                    for (int r = 0; r < R; r++) {
-                        const int d = r * 32 + lane;
-                        v[r] = d < nu ? ((__ldcg(dist + d) << 8) | (uint32_t)d) : kEmpty;
+            for (int k = 0; k < EA; k++) early[k] = lane + 32 * k < n ? (uint32_t)__ldcg(amap + lane + 32 * k) : 0u;
+            // R distinct ids per lane, d = lane * R + r (16-byte loads; words past nu stay inside the batch's area)
+            auto run = [&](auto rtag) {
+                constexpr int R = decltype(rtag)::value;
+                uint32_t v[R];
+                if (R >= 4) {
+#pragma unroll
+                    for (int r = 0; r < R; r += 4) {
+                        uint4 x = make_uint4(0, 0, 0, 0);
+                        if (lane * R + r < nu) x = __ldcg(reinterpret_cast<const uint4*>(dist + lane * R + r));
+                        v[r] = x.x; v[r + 1 < R ? r + 1 : r] = x.y; v[r + 2 < R ? r + 2 : r] = x.z; v[r + 3 < R ? r + 3 : r] = x.w;
                     }
-                    warp_bitonic_regs<R>(v, lane);
+                } else {
 #pragma unroll
-                    for (int r = 0; r < R; r++) {
-                        const int j = r * 32 + lane;
-                        if (j < nu) {
-                            list[j] = v[r] >> 8;
-                            of_d[v[r] & 0xFFu] = (uint16_t)j;
+                    for (int r = 0; r < R; r++) v[r] = lane * R + r < nu ? __ldcg(dist + lane * R + r) : 0u;
+                }
+                if (want_pos && g.prefetch) {  // the vertices on their way to L2 while the list is put in order
+#pragma unroll
+                    for (int r = 0; r < R; r++)
+                        if (lane * R + r < nu && vertex_in_range(sp, (uint32_t)vbase + v[r])) prefetch_l2(sp.pos4 + vbase + v[r]);
+                }
+                if (STRATEGY == VR_SORT) {
+                    // ascending ids: sort id << 8 | d; position j holds the j-th smallest id and says which d it was
+#pragma unroll
+                    for (int r = 0; r < R; r++) v[r] = lane * R + r < nu ? ((v[r] << 8) | (uint32_t)(lane * R + r)) : kEmpty;
+                    warp_bitonic_blocked<R>(v, lane);
+                    // (the list leaves the registers as 16-byte stores: word stores at a stride of R words would be
+                    // R-way bank conflicts; entries past nu are never read)
+                    if (R >= 4) {
+#pragma unroll
+                        for (int r = 0; r < R; r += 4)
+                            *reinterpret_cast<uint4*>(list + lane * R + r) =
+                                make_uint4(v[r] >> 8, v[r + 1 < R ? r + 1 : r] >> 8, v[r + 2 < R ? r + 2 : r] >> 8, v[r + 3 < R ? r + 3 : r] >> 8);
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < R; r++) list[lane * R + r] = v[r] >> 8;
+                    }
+#pragma unroll
+                    for (int r = 0; r < R; r++)
+                        if (lane * R + r < nu) of_d[v[r] & 0xFFu] = (uint16_t)(lane * R + r);
+                } else {
+                    const int stride = dyn3_aux_stride(n);
+                    const unsigned char* __restrict__ aux = g.aux + dyn3_aux_base(c, b, mo);
+                    const unsigned char* __restrict__ home = aux + kDyn3AuxHome;
+                    const unsigned char* __restrict__ slot = home + stride;
+                    uint32_t* bm = s_bm[wid];
+                    {  // occupancy words of the table and their exclusive popcount prefix
+                        const uint32_t wv = lane < 8 ? __ldcg(reinterpret_cast<const uint32_t*>(aux) + lane) : 0u;
+                        const int inc = warp_incl_scan(__popc(wv), lane);
+                        if (lane < 8) { bm[lane] = wv; bm[8 + lane] = (uint32_t)(inc - __popc(wv)); }
+                    }
+                    uint32_t sl[R], hm[R];
+                    if (R == 8) {  // 8 slots / home slots of a lane: one 8-byte load each (rows past nu stay inside the batch's area)
+                        const uint2 sv = lane * R < nu ? __ldcg(reinterpret_cast<const uint2*>(slot + lane * R)) : make_uint2(0, 0);
+                        const uint2 hv = lane * R < nu ? __ldcg(reinterpret_cast<const uint2*>(home + lane * R)) : make_uint2(0, 0);
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            sl[r] = ((r < 4 ? sv.x : sv.y) >> (8 * (r & 3))) & 0xFFu;
+                            hm[r] = ((r < 4 ? hv.x : hv.y) >> (8 * (r & 3))) & 0xFFu;
+                        }
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < R; r++) {
+                            const int d = lane * R + r;
+                            sl[r] = d < nu ? (uint32_t)__ldcg(slot + d) : 0u;
+                            hm[r] = d < nu ? (uint32_t)__ldcg(home + d) : 0u;
                         }
                     }
-                };
-                if (nu <= 32) run(std::integral_constant<int, 1>{});
-                else if (nu <= 64) run(std::integral_constant<int, 2>{});
-                else if (nu <= 128) run(std::integral_constant<int, 4>{});
-                else run(std::integral_constant<int, 8>{});
-            } else {
-                const int stride = dyn3_aux_stride(n);
-                const unsigned char* __restrict__ home = g.aux + dyn3_aux_base(c, b, mo);
-                const unsigned char* __restrict__ slot = home + stride;
-                uint32_t* bm = s_bm[wid];
-                if (lane < 16) bm[lane] = 0;
-                __syncwarp();
-                uint32_t sl[8], hm[8], idv[8];
+                    __syncwarp();
+                    const uint32_t tmask = c.table_size - 1;
+                    uint32_t e[R];
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int d = r * 32 + lane;
-                    sl[r] = d < nu ? (uint32_t)__ldcg(slot + d) : 0u;
-                    hm[r] = d < nu ? (uint32_t)__ldcg(home + d) : 0u;
-                    idv[r] = d < nu ? __ldcg(dist + d) : 0u;
-                    if (d < nu) atomicOr(&bm[sl[r] >> 5], 1u << (sl[r] & 31));
-                }
-                __syncwarp();
-                {  // exclusive popcount prefix of the 8 occupancy words -> bm[8..16)
-                    const uint32_t wv = lane < 8 ? bm[lane] : 0u;
-                    const int inc = warp_incl_scan(__popc(wv), lane);
-                    if (lane < 8) bm[8 + lane] = (uint32_t)(inc - __popc(wv));
-                }
-                __syncwarp();
-                const uint32_t tmask = c.table_size - 1;
+                    for (int r = 0; r < R; r++) {
+                        const int d = lane * R + r;
+                        e[r] = 0;
+                        if (d < nu) {  // strategies.py:370-380: rank of the slot among the occupied ones
+                            const uint32_t wi = sl[r] >> 5;
+                            const uint32_t j = bm[8 + wi] + (uint32_t)__popc(bm[wi] & ((1u << (sl[r] & 31)) - 1u));
+                            list[j] = v[r];
+                            e[r] = (((sl[r] - hm[r]) & tmask) << 8) | j;
+                        }
+                    }
+                    if (R == 8) {
+                        *reinterpret_cast<uint4*>(of_d + lane * R) =
+                            make_uint4(e[0] | (e[1] << 16), e[2 % R] | (e[3 % R] << 16), e[4 % R] | (e[5 % R] << 16), e[6 % R] | (e[7 % R] << 16));
+                    } else {
 #pragma unroll
-                for (int r = 0; r < 8; r++) {
-                    const int d = r * 32 + lane;
-                    if (d < nu) {  // strategies.py:370-380: rank of the slot among the occupied ones
-                        const uint32_t wi = sl[r] >> 5;
-                        const uint32_t j = bm[8 + wi] + (uint32_t)__popc(bm[wi] & ((1u << (sl[r] & 31)) - 1u));
-                        list[j] = idv[r];
-                        of_d[d] = (uint16_t)((((sl[r] - hm[r]) & tmask) << 8) | j);
+                        for (int r = 0; r < R; r++) of_d[lane * R + r] = (uint16_t)e[r];
                     }
                 }
-            }
+            };
+            if (nu <= 32) run(std::integral_constant<int, 1>{});
+            else if (nu <= 64) run(std::integral_constant<int, 2>{});
+            else if (nu <= 128) run(std::integral_constant<int, 4>{});
+            else run(std::integral_constant<int, 8>{});
             __syncwarp();
             // local indices (and the probe statistics of every element, duplicates included)
-            uint16_t* __restrict__ amap = c.out.d_assembly_map + mo;
             unsigned int fast = 0, slow = 0, cmax = 0;
             const int wshift = ilog2((uint32_t)g.w);
-            for (int i = lane; i < n; i += 32) {
-                const uint32_t e = of_d[amap[i] & 0xFFu];
+            auto element = [&](int i, uint32_t dnum) {
+                const uint32_t e = of_d[dnum & 0xFFu];
                 amap[i] = (uint16_t)(e & 0xFFu);
                 if (STRATEGY != VR_SORT) {
                     const uint32_t dd = e >> 8;  // chain - 1 (strategies.py:277-297)
@@ -371,7 +501,11 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_finish_kernel(RunCtx c, 
                     }
                     cmax = max(cmax, dd + 1);
                 }
-            }
+            };
+#pragma unroll
+            for (int k = 0; k < EA; k++)
+                if (lane + 32 * k < n) element(lane + 32 * k, early[k]);
+            for (int i = lane + 32 * EA; i < n; i += 32) element(i, amap[i]);
             if (STRATEGY != VR_SORT) {
                 fast = __reduce_add_sync(0xffffffffu, fast);
                 slow = __reduce_add_sync(0xffffffffu, slow);
@@ -382,7 +516,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_finish_kernel(RunCtx c, 
                     atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)cmax);
                 }
             }
-            shade_stream<VR_SORT>(c, sp, list, nu, off.y, lane, 32, mo, sp.batch_base ? __ldg(sp.batch_base + b) : 0, b);
+            shade_stream<VR_SORT>(c, sp, list, nu, off.y, lane, 32, mo, vbase, b);
         }
     }
     // the last CTA to finish writes the statistics block (every CTA's probe counts are in by then)
@@ -423,7 +557,7 @@ static Dyn3Plan dyn3_plan(int strategy, const vr_batch_config* cfg, const vr_has
     if (g.u_bound > 256) return p;
     g.q = (int)next_pow2((uint32_t)((g.u_bound + 32) * 3 / 2 + 2));  // the set holds <= u_bound + 32 ids: load <= 2/3
     if (g.q < 128) g.q = 128;
-    g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4 + 2);
+    g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4);
     p.smem_a = (size_t)kDyn3Warps * g.per_warp_bytes;
     p.ok = true;
     return p;

@@ -588,11 +588,12 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     const int n_tiles = (int)ceil_div(n, L.tile);
     // tile version: thread per position, counting sort by table slot (16-bit relative positions)
     const int halo2 = (L.window + 31) & ~31;
-    const int tile2 = getenv("VR_LINK_TILE") ? atoi(getenv("VR_LINK_TILE")) : 2048;  // (4096 / 6144: fewer CTAs per SM, measured slower)
+    const DebugKnobs& knobs = debug_knobs();
+    const int tile2 = knobs.link_tile;  // (4096 / 6144: fewer CTAs per SM, measured slower)
     const int np2 = tile2 + halo2;
     const int nslots2 = (int)next_pow2((uint32_t)(np2 + np2 / 3));  // load <= 0.75
     const size_t smem2 = (size_t)nslots2 * 4 + (size_t)(nslots2 + 1) * 4 + (size_t)np2 * 4 + 16;
-    if (np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !getenv("VR_LINKS_WARP")) {
+    if (np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !knobs.links_warp) {
         VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
         occurrence_links_tile_kernel<<<(int)ceil_div(n, tile2), kLinkThreads, smem2, stream>>>(c, tile2, halo2, nslots2);
     } else if (small_last) {
@@ -602,7 +603,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
         VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         occurrence_links_kernel<int32_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
     }
-    const int run = getenv("VR_GREEDY_RUN") ? atoi(getenv("VR_GREEDY_RUN")) : 64;
+    const int run = knobs.greedy_run;
     const int n_threads = (int)ceil_div(L.T, run);
     // shared-memory version when a CTA's stretch (128 runs + one batch window) fits as 16-bit distances
     // (run * ps halfwords between the lanes' streams: an odd number of 32-bit words keeps their reads on
@@ -610,7 +611,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     int run_s = 30;
     while ((run_s * c.ps) % 4 != 2 && run_s < 33) run_s++;
     const int64_t npos_s = (int64_t)128 * run_s * c.ps + L.window + c.ps;
-    if (npos_s * 4 <= 56 * 1024 && L.window < 60000 && !getenv("VR_GREEDY_GLOBAL")) {
+    if (npos_s * 4 <= 56 * 1024 && L.window < 60000 && !knobs.greedy_global) {
         VR_CUDA_CHECK(cudaFuncSetAttribute(greedy_next_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(npos_s * 4)));
         greedy_next_smem_kernel<<<(int)ceil_div(L.T, 128 * run_s), 128, (size_t)npos_s * 4, stream>>>(c, run_s, (int)npos_s);
     } else {
@@ -621,7 +622,7 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     // B3 / B4: rows of 8 tables at a time through shared memory when they fit
     int walk_rows = 8;
     while (walk_rows > 1 && (size_t)walk_rows * L.cap * 8 > 48 * 1024) walk_rows >>= 1;
-    const bool walk_smem = (size_t)walk_rows * L.cap * 8 <= 48 * 1024 && walk_rows >= 2 && !getenv("VR_WALK_GLOBAL");
+    const bool walk_smem = (size_t)walk_rows * L.cap * 8 <= 48 * 1024 && walk_rows >= 2 && !knobs.walk_global;
     if (walk_smem) table_walk_kernel<<<1, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 0, walk_rows);
     else group_scan_kernel<<<1, 32, 0, stream>>>(c);
     if (c.draw_start) draws_check_kernel<<<(n_draws + 256) / 256, 256, 0, stream>>>(c);

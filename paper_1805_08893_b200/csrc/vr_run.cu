@@ -1452,6 +1452,7 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
     const bool want_pos = sp.kind == VR_SHADER_POSITION;
     const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
     const bool want_cnt = c.out.d_shade_counts != nullptr;
+    const L2Policies pol = make_l2_policies();
     uint32_t* __restrict__ out_uid = c.out.d_unique_ids + dst0;
     float4* __restrict__ shaded = reinterpret_cast<float4*>(c.out.d_shaded4) + dst0;
     for (int j0 = 0; j0 < cnt; j0 += width * kShadeUnroll) {
@@ -1468,15 +1469,15 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
         if (want_pos) {
 #pragma unroll
             for (int u = 0; u < kShadeUnroll; u++)
-                if (live[u]) p[u] = __ldg(sp.pos4 + vbase + uid[u]);
+                if (live[u]) p[u] = ldg_keep_f4(sp.pos4 + vbase + uid[u], pol.keep);
         }
 #pragma unroll
         for (int u = 0; u < kShadeUnroll; u++) {
             const int j = j0 + u * width + l;
             if (j >= cnt) continue;
-            if (want_uid) out_uid[j] = uid[u];
+            if (want_uid) st_stream_u32(out_uid + j, uid[u], pol.stream);
             if (!live[u]) continue;
-            if (want_pos) shaded[j] = transform_position(sp, p[u]);
+            if (want_pos) st_stream_f4(shaded + j, transform_position(sp, p[u]), pol.stream);
             if (STRATEGY == VR_NAIVE && c.out.d_assembly_map) c.out.d_assembly_map[naive_mo + j] = (uint16_t)(j % c.ps);
             if (want_attr)
                 for (int k = 0; k < sp.attr_words; k++)
@@ -1967,7 +1968,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     Dyn3Plan d3 = dyn3_plan(strategy, cfg, hc, max_span, c.enforce_budget != 0, shader, out);
     if (!allow_fuse || nb == 0 || nb >= (1 << 30)) d3.ok = false;
     d3.g.aux = ws + L.aux;
-    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, kDyn3Warps) : 0;
+    d3.g.prefetch = debug_knobs().dyn3_prefetch;
+    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, kDyn3Tile) : 0;
     g_prof_marks = 0;
     g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : d3.ok ? 4 : 0;
     prof_mark(stream);
@@ -1979,7 +1981,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         if (strategy == VR_NAIVE) {
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
         } else if (d3.ok) {
-            const int tiles = c.n_fused_tiles;
+            const int tiles = c.n_fused_tiles, ftiles = (int)ceil_div(nb, kDyn3Warps);
             if (strategy == VR_SORT) {
                 VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
                 dyn3_dedup_kernel<false, false><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
@@ -1990,14 +1992,14 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             } else {
                 VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
                 dyn3_dedup_kernel<true, true><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
-                dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads), kDyn3InsertThreads, 0, stream>>>(c, d3.g);
+                dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads / 2), kDyn3InsertThreads / 2, 0, stream>>>(c, d3.g);
             }
             prof_mark(stream);
             prof_mark(stream);
             switch (strategy) {
-            case VR_SORT: dyn3_finish_kernel<VR_SORT><<<tiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
-            case VR_HASH: dyn3_finish_kernel<VR_HASH><<<tiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
-            default: dyn3_finish_kernel<VR_PHASH><<<tiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            case VR_SORT: dyn3_finish_kernel<VR_SORT><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            case VR_HASH: dyn3_finish_kernel<VR_HASH><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            default: dyn3_finish_kernel<VR_PHASH><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
             }
             prof_mark(stream);
             g_last_launches = strategy == VR_SORT ? 3 : 4;
@@ -2051,7 +2053,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             // (a few long batches -- configs[0]: 509 batches of 768 -- do not fill the GPU with one warp each:
             // the CTA sort is faster there)
             const bool few_long = nb < 2048 && wp > 512;
-            if (per_warp <= 24 * 1024 && wq <= 65536 && !few_long && !getenv("VR_SORT_CTA")) {
+            if (per_warp <= 24 * 1024 && wq <= 65536 && !few_long && !debug_knobs().sort_cta) {
                 int warps = 8;
                 while (warps > 1 && warps * per_warp > 64 * 1024) warps >>= 1;
                 const size_t wsmem = (size_t)warps * per_warp;

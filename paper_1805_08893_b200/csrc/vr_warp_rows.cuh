@@ -691,8 +691,8 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
     // Optional: prefetch the vertices of a tile into L2 when it is deduplicated (VR_PREFETCH=1).  Off by
     // default: on the B200 the gathers ~K tiles later are L2 hits or overlap the next tile's dedup
     // anyway, and the extra L2 requests cost more than they save (profiles/README.md).
-    const char* pf = getenv("VR_PREFETCH");
-    const bool prefetch = sp.kind == VR_SHADER_POSITION && pf && pf[0] == '1';
+    const DebugKnobs& knobs = debug_knobs();
+    const bool prefetch = sp.kind == VR_SHADER_POSITION && knobs.rows_prefetch == 1;
     auto kernel = prefetch ? warp_rows_kernel<W, true> : warp_rows_kernel<W, false>;
     RowsGeom g = g_in;
     VR_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem));
@@ -702,13 +702,12 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRowCtaThreads, g.smem);
     g.n_tiles = (int)ceil_div(c.n_batches, kRowThreads);
     g.n_groups = (int)ceil_div(g.n_tiles, kRowGroup);
-    const char* e = getenv("VR_LAG");
     const int resident = sms * (per_sm > 0 ? per_sm : 1);
     // Tickets go round the persistent CTAs, so tile i - resident is the CTA's own previous tile and its
     // predecessors are being published by the other CTAs just now: with K = 1.5 x resident every
     // aggregate the look-back needs is half a round old and nothing waits.  A longer lag only
     // lengthens the shade-only tail (measured: 0.138 / 0.131 / 0.128 / 0.134 ms at 1.0 / 1.25 / 1.5 / 2.0).
-    g.lag = e ? atoi(e) : resident + resident / 2;
+    g.lag = knobs.rows_lag > 0 ? knobs.rows_lag : resident + resident / 2;
     if (g.lag > g.n_tiles) g.lag = g.n_tiles;
     if (g.lag < 1) g.lag = 1;
     const int tickets = g.n_tiles + g.lag;  // the last `lag` tickets only shade
@@ -721,7 +720,7 @@ static int launch_warp_rows(const RunCtx& c, int bs, const RowsGeom& g_in, const
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap init_kernel's tail
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = getenv("VR_NO_PDL") ? 0 : 1;
+    cfg.numAttrs = knobs.no_pdl ? 0 : 1;
     VR_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, c, bs, g, sp));
     return VR_OK;
 }
