@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define VRGEOM_ABI_VERSION 2
+#define VRGEOM_ABI_VERSION 3
 
 /* strategies.py:387  STRATEGY_NAMES = ("naive", "warp", "sort", "hash", "phash") */
 enum vr_strategy {
@@ -115,6 +115,9 @@ typedef struct vr_shader {
                                   shader reads positions/attributes at base + id and tallies
                                   d_shade_counts[base + id]; unique ids stay draw-local, as the
                                   reference's per-draw runs report them.  NULL = one vertex buffer */
+    int32_t extra_cycles;      /* synthetic shader load ("256/512/1024 cycles"; ShaderFn.cycles,
+                                  strategies.py:40-44): a dependent chain of this many FP32 FMAs per
+                                  invocation that leaves the record unchanged.  0 = the plain transform */
 } vr_shader;
 
 /* Statistics block: int64[VR_STATS_WORDS] in device memory, written by vr_run.
@@ -214,6 +217,63 @@ int vr_expand_stream(const int32_t *d_batch_round_off, const int32_t *d_round_ui
                      const int32_t *d_batch_begin, const int32_t *d_batch_end, int32_t primitive_size,
                      float *d_stream_pos3, uint32_t *d_stream_ids, void *d_workspace,
                      size_t workspace_bytes, void *stream);
+
+/* Same walk as vr_expand_stream, but out[slot] = round base + assembly_map[slot]: the position of the
+ * slot's record in the unique-id / shaded arrays (int32[n_slots]).  Clients that attach their own
+ * per-unique payload (the random-walk client below) expand it with this. */
+int vr_expand_sources(const int32_t *d_batch_round_off, const int32_t *d_round_uid_off,
+                      const int32_t *d_round_prims, const uint16_t *d_assembly_map, int64_t n_batches,
+                      const int32_t *d_batch_begin, const int32_t *d_batch_end, int32_t primitive_size,
+                      int32_t *d_stream_src, void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* analytics.py:105-119 ideal_report: one invocation per REFERENCED vertex.  d_counts is int32[vertex_count]
+ * (1 for a referenced vertex, else 0); d_out is device int64[2]: [0] the number of referenced vertices,
+ * [1] a vr_status found on the device (VR_ERR_VERTEX_RANGE for an index outside the buffer). */
+int vr_ideal_counts(const uint32_t *d_indices, int64_t n_indices, int32_t vertex_count, int32_t *d_counts,
+                    int64_t *d_out, void *stream);
+
+/* cache.py:66-130 simulate_parallel_cache: per-multiprocessor LRU post-transform cache with the concurrency
+ * penalty of wide hardware (duplicates arriving in one wave all miss).  The buffer is cut into
+ * num_processors primitive-aligned chunks (cache.py:88-90), one CTA each; a wave of wave_width indices is
+ * looked up against the cache as it stood before the wave, hits refresh recency in wave order, the wave's
+ * missed ids are inserted in first-miss order afterwards and the least recently used entries leave while the
+ * cache is over capacity (cache.py:106-129).  d_out is device int64[4]: hits, misses, vr_status, 0.
+ * d_miss_counts (int32[vertex_count], zeroed by the caller) receives one count per miss, or NULL. */
+typedef struct vr_cache_config {
+    int32_t num_processors; /* cache.py:29 default 28   */
+    int32_t wave_width;     /* cache.py:30 default 1024 */
+    int32_t capacity;       /* cache.py:43-47 entries   */
+    int32_t primitive_size;
+} vr_cache_config;
+size_t vr_cache_workspace_bytes(int64_t n_indices, const vr_cache_config *cfg);
+int vr_simulate_cache(const uint32_t *d_indices, int64_t n_indices, const vr_cache_config *cfg,
+                      int32_t vertex_count, int32_t *d_miss_counts, int64_t *d_out, void *d_workspace,
+                      size_t workspace_bytes, void *stream);
+
+/* ---- random-walk client (walk.py) ------------------------------------------------------
+ * Agents on a grid, positions packed as virtual indices (y << 16 | x, walk.py:75-82) and run through vr_run
+ * with primitive_size 1, so that agents sharing a cell share one likelihood evaluation per batch. */
+#define VR_WALK_MAX_GAUSSIANS 8
+typedef struct vr_walk_config {   /* walk.py:51-72 WalkConfig */
+    int32_t grid_w, grid_h;
+    int32_t max_move_distance;
+    int32_t kept_moves;
+    int32_t n_gaussians;
+    int32_t reserved;
+    double gaussians[VR_WALK_MAX_GAUSSIANS][4]; /* walk.py:32-36: center x, center y, sigma, amplitude */
+} vr_walk_config;
+/* walk.py:110-137 cell_likelihoods for n cells: d_moves is double[n][kept_moves][3] = (dx, dy, likelihood),
+ * descending likelihood, ties in row-major scan order; FP64.  d_status is device int64[1] (0 or
+ * (cell index << 8) | VR_ERR_BAD_CONFIG when a cell has fewer legal moves than kept_moves, walk.py:123-126). */
+int vr_walk_likelihoods(const uint32_t *d_cells, int64_t n_cells, const vr_walk_config *cfg, double *d_moves,
+                        int64_t *d_status, void *stream);
+/* walk.py:140-165 + :202-207: agent a draws u = agent_uniforms(seed, step, a) (splitmix64), picks move
+ * choose_move(moves[src[a]], u) and advances.  Positions are int32 (x, y) pairs; d_src is the output of
+ * vr_expand_sources (NULL: agent a uses record a -- the per-agent path of walk.py:210-219). */
+int vr_walk_advance(const int32_t *d_positions_in, int64_t n_agents, const int32_t *d_src, const double *d_moves,
+                    int32_t kept_moves, uint64_t seed, int64_t step, int32_t *d_positions_out, void *stream);
+/* walk.py:167-170 pack_positions on the device: cells[a] = y << 16 | x. */
+int vr_walk_pack(const int32_t *d_positions, int64_t n_agents, uint32_t *d_cells, void *stream);
 
 /* Profiling aid (bench.py): per-kernel device time of the last vr_run, measured with CUDA
  * events on the launching stream.  Stages, in order: init (+ span scan), dedup, offset scan

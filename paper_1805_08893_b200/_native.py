@@ -7,7 +7,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvrgeom.so")
-ABI_VERSION = 2  # VRGEOM_ABI_VERSION of include/vrgeom.h this binding was written against
+ABI_VERSION = 3  # VRGEOM_ABI_VERSION of include/vrgeom.h this binding was written against
 
 VR_NAIVE, VR_WARP, VR_SORT, VR_HASH, VR_PHASH = range(5)
 STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_HASH, "phash": VR_PHASH}
@@ -52,7 +52,7 @@ class HashConfigC(C.Structure):
 class ShaderC(C.Structure):
     _fields_ = [("kind", C.c_int32), ("has_matrix", C.c_int32), ("matrix", C.c_float * 16),
                 ("d_positions4", C.c_void_p), ("d_attributes", C.c_void_p), ("attr_words", C.c_int32),
-                ("vertex_count", C.c_int32), ("d_batch_vertex_base", C.c_void_p)]
+                ("vertex_count", C.c_int32), ("d_batch_vertex_base", C.c_void_p), ("extra_cycles", C.c_int32)]
 
 
 class OutputsC(C.Structure):
@@ -61,6 +61,20 @@ class OutputsC(C.Structure):
                 ("d_assembly_map", C.c_void_p), ("d_shaded4", C.c_void_p),
                 ("d_shaded_attr", C.c_void_p), ("d_shade_counts", C.c_void_p), ("d_stats", C.c_void_p),
                 ("cap_unique", C.c_int64), ("cap_rounds", C.c_int64)]
+
+
+class CacheConfigC(C.Structure):
+    _fields_ = [("num_processors", C.c_int32), ("wave_width", C.c_int32), ("capacity", C.c_int32),
+                ("primitive_size", C.c_int32)]
+
+
+VR_WALK_MAX_GAUSSIANS = 8
+
+
+class WalkConfigC(C.Structure):
+    _fields_ = [("grid_w", C.c_int32), ("grid_h", C.c_int32), ("max_move_distance", C.c_int32),
+                ("kept_moves", C.c_int32), ("n_gaussians", C.c_int32), ("reserved", C.c_int32),
+                ("gaussians", (C.c_double * 4) * VR_WALK_MAX_GAUSSIANS)]
 
 
 _lib = None
@@ -94,6 +108,16 @@ _SIGNATURES = {
     "vr_expand_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_expand_sources": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                    C.c_int32, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_ideal_counts": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vr_cache_workspace_bytes": (C.c_size_t, [C.c_int64, C.POINTER(CacheConfigC)]),
+    "vr_simulate_cache": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(CacheConfigC), C.c_int32, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_walk_likelihoods": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(WalkConfigC), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vr_walk_advance": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_uint64, C.c_int64,
+                                  C.c_void_p, C.c_void_p]),
+    "vr_walk_pack": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
 }
 
 

@@ -1,6 +1,6 @@
 """Reuse statistics contract of the hot path (host mirror of `vrlab/analytics.py`,
 /root/reference/pkg/src/vrlab/analytics.py:20-50 `ReuseReport`, :74-102 `build_report`).
-Tables, CSV/JSON writers and cost estimates are out of scope."""
+`ideal_report` :105-119 runs on the device.  Tables and CSV/JSON writers are out of scope."""
 from __future__ import annotations
 
 from dataclasses import dataclass
@@ -54,9 +54,27 @@ def build_report(*, scene: str, strategy: str, indices: int, invocations: int, b
                        reuse_rate=reuse, batches=batches, per_vertex=per_vertex, probe_stats=probe_stats)
 
 
-def ideal_reuse(indices) -> float:
-    """1 - unique/len, the reuse ceiling (cache.py:58-63)."""
-    idx = np.asarray(indices)
-    if len(idx) == 0:
+def ideal_report(mesh, scene: str = "") -> ReuseReport:
+    """Reuse ceiling: one invocation per referenced vertex (analytics.py:105-119), counted on the device
+    (vr_ideal_counts)."""
+    from . import engine
+
+    if len(mesh.indices) == 0:
         raise ValueError("empty index buffer")
-    return 1.0 - len(np.unique(idx)) / len(idx)
+    referenced, counts = engine.ideal_counts(engine.to_device_indices(mesh.indices), mesh.vertex_count)
+    return build_report(scene=scene, strategy="ideal", indices=len(mesh.indices), invocations=referenced,
+                        batches=1, shade_counts=counts.cpu().numpy().astype(np.int64))
+
+
+@dataclass(frozen=True)
+class CostEstimate:
+    """analytics.py:53-71: abstract cost = invocations x ShaderFn.cycles."""
+
+    invocations: int
+    cycles_per_invocation: int
+    total_cycles: int
+
+
+def estimate_cost(report: ReuseReport, shader) -> CostEstimate:
+    return CostEstimate(invocations=report.invocations, cycles_per_invocation=shader.cycles,
+                        total_cycles=report.invocations * shader.cycles)

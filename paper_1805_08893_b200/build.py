@@ -6,7 +6,7 @@ import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(_HERE, "csrc")
-SOURCES = ("vr_run.cu", "vr_dynamic.cu")
+SOURCES = ("vr_run.cu", "vr_dynamic.cu", "vr_clients.cu")
 LIB = os.path.join(_HERE, "libvrgeom.so")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "--use_fast_math=false"]

@@ -121,6 +121,8 @@ struct ShaderParams {
     int attr_words;
     int vertex_count;
     const int32_t* __restrict__ batch_base;  // multi-draw: first vertex of each batch's draw, or NULL
+    int extra_cycles;   // synthetic shader load: dependent FMAs per invocation (vr_shader.extra_cycles)
+    float load_a, load_b;  // 1, 0 at run time (kernel parameters, so the chain is not folded away)
 };
 
 // L2 eviction policies (createpolicy + .L2::cache_hint): a random 16-byte gather pulls a 32-byte sector, so a
@@ -147,15 +149,27 @@ __device__ __forceinline__ void st_stream_u32(uint32_t* p, uint32_t v, unsigned 
 
 // The w-divide uses one hardware reciprocal (MUFU.RCP, <= 1 ulp) and three multiplies: a few ulp
 // of FP32 from the reference's float64 result, far inside the 1e-5 relative bound.
+// LOAD: honour sp.extra_cycles (the general shading kernels); the fused warp-voting kernels are compiled without it
+// and vr_run does not select them for a loaded shader.
+template <bool LOAD = false>
 __device__ __forceinline__ float4 transform_position(const ShaderParams& sp, float4 p) {
-    if (!sp.has_matrix) return make_float4(p.x, p.y, p.z, 1.0f);
+    if (!sp.has_matrix) {
+        float w = 1.0f;
+        if (LOAD)
+            for (int k = 0; k < sp.extra_cycles; k++) w = fmaf(w, sp.load_a, sp.load_b);
+        return make_float4(p.x, p.y, p.z, w);
+    }
     const float ox = fmaf(sp.m[0], p.x, fmaf(sp.m[1], p.y, fmaf(sp.m[2], p.z, sp.m[3])));
     const float oy = fmaf(sp.m[4], p.x, fmaf(sp.m[5], p.y, fmaf(sp.m[6], p.z, sp.m[7])));
     const float oz = fmaf(sp.m[8], p.x, fmaf(sp.m[9], p.y, fmaf(sp.m[10], p.z, sp.m[11])));
     const float ow = fmaf(sp.m[12], p.x, fmaf(sp.m[13], p.y, fmaf(sp.m[14], p.z, sp.m[15])));
     float iw;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(iw) : "f"(ow));
-    return make_float4(ox * iw, oy * iw, oz * iw, ow);
+    float w = ow;
+    // the paper's synthetic shader loads: a dependent chain w = w * 1 + 0, exact, one FMA per "cycle"
+    if (LOAD)
+        for (int k = 0; k < sp.extra_cycles; k++) w = fmaf(w, sp.load_a, sp.load_b);
+    return make_float4(ox * iw, oy * iw, oz * iw, w);
 }
 
 }  // namespace vr

@@ -1477,7 +1477,7 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
             if (j >= cnt) continue;
             if (want_uid) st_stream_u32(out_uid + j, uid[u], pol.stream);
             if (!live[u]) continue;
-            if (want_pos) st_stream_f4(shaded + j, transform_position(sp, p[u]), pol.stream);
+            if (want_pos) st_stream_f4(shaded + j, transform_position<true>(sp, p[u]), pol.stream);
             if (STRATEGY == VR_NAIVE && c.out.d_assembly_map) c.out.d_assembly_map[naive_mo + j] = (uint16_t)(j % c.ps);
             if (want_attr)
                 for (int k = 0; k < sp.attr_words; k++)
@@ -1561,7 +1561,7 @@ __global__ void __launch_bounds__(kShadeThreads) shade_kernel(RunCtx c, ShaderPa
                 if (j >= tot) continue;
                 if (want_uid) out_uid[j] = uid[u];
                 if (!live[u]) continue;
-                if (want_pos) shaded[j] = transform_position(sp, p[u]);
+                if (want_pos) shaded[j] = transform_position<true>(sp, p[u]);
                 if (want_attr)
                     for (int k = 0; k < sp.attr_words; k++)
                         c.out.d_shaded_attr[((int64_t)off.y + j) * sp.attr_words + k] = __ldg(sp.attr + ((int64_t)vb[u] + uid[u]) * sp.attr_words + k);
@@ -1601,7 +1601,8 @@ __global__ void __launch_bounds__(256) expand_kernel(const int32_t* __restrict__
                                                       const int32_t* __restrict__ rprims, const uint16_t* __restrict__ amap,
                                                       const uint32_t* __restrict__ uids, const float4* __restrict__ shaded,
                                                       int n_batches, const int32_t* __restrict__ map_off, int ps,
-                                                      float* __restrict__ out_pos3, uint32_t* __restrict__ out_ids) {
+                                                      float* __restrict__ out_pos3, uint32_t* __restrict__ out_ids,
+                                                      int32_t* __restrict__ out_src) {
     const int lane = threadIdx.x & 31;
     const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (b >= n_batches) return;
@@ -1611,6 +1612,7 @@ __global__ void __launch_bounds__(256) expand_kernel(const int32_t* __restrict__
         const int slots = rprims[r] * ps;
         for (int k = lane; k < slots; k += 32) {
             const int src = base + amap[m + k];
+            if (out_src) out_src[m + k] = src;
             if (out_ids) out_ids[m + k] = uids[src];
             if (out_pos3) {
                 float4 v = shaded[src];
@@ -1934,6 +1936,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         sp.pos4 = (const float4*)shader->d_positions4; sp.attr = shader->d_attributes;
         sp.attr_words = shader->d_attributes ? shader->attr_words : 0; sp.vertex_count = shader->vertex_count;
         sp.batch_base = shader->d_batch_vertex_base;
+        sp.extra_cycles = shader->extra_cycles > 0 ? shader->extra_cycles : 0;
+        sp.load_a = 1.0f; sp.load_b = 0.0f;
         if (sp.kind == VR_SHADER_POSITION && (!sp.pos4 || !out->d_shaded4)) return VR_ERR_BAD_CONFIG;
     }
     const int nbi = (int)nb;
@@ -1957,7 +1961,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
 
     // (the position-aligned kernels read one vertex buffer: multi-draw runs take the general path)
     const bool fast_warp = strategy == VR_WARP && static_batches && ps == 3 && cfg->batch_size % 8 == 0 && nb > 0 && !sp.batch_base;
-    const bool fused = fast_warp && allow_fuse;
+    const bool fused = fast_warp && allow_fuse && sp.extra_cycles == 0;  // (the fused kernels shade without the synthetic load)
     // tile kernel (vr_warp_rows.cuh) when a batch row fits shared memory comfortably
     RowsGeom rg{};
     // (its packed table entries hold 24-bit ids: the caller must state a vertex count that fits)
@@ -2146,7 +2150,23 @@ int vr_expand_stream(const int32_t* d_bro, const int32_t* d_ruo, const int32_t* 
     int32_t* map_off = (int32_t*)d_ws;
     span_only_scan_kernel<<<1, 1024, 0, stream>>>(d_bbegin, d_bend, (int)nb, map_off);
     expand_kernel<<<(int)ceil_div(nb, 8), 256, 0, stream>>>(d_bro, d_ruo, d_rprims, d_amap, d_uids,
-                                                             (const float4*)d_shaded4, (int)nb, map_off, ps, d_pos3, d_ids);
+                                                             (const float4*)d_shaded4, (int)nb, map_off, ps, d_pos3, d_ids, nullptr);
+    VR_CUDA_CHECK(cudaGetLastError());
+    return VR_OK;
+}
+
+int vr_expand_sources(const int32_t* d_bro, const int32_t* d_ruo, const int32_t* d_rprims, const uint16_t* d_amap, int64_t nb,
+                      const int32_t* d_bbegin, const int32_t* d_bend, int32_t ps, int32_t* d_src, void* d_ws, size_t ws_bytes,
+                      void* stream_) {
+    if (nb <= 0) return VR_OK;
+    if (ws_bytes < (size_t)(nb + 1) * 4 || !d_ws) return VR_ERR_WORKSPACE;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (!d_src) return VR_ERR_BAD_CONFIG;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    int32_t* map_off = (int32_t*)d_ws;
+    span_only_scan_kernel<<<1, 1024, 0, stream>>>(d_bbegin, d_bend, (int)nb, map_off);
+    expand_kernel<<<(int)ceil_div(nb, 8), 256, 0, stream>>>(d_bro, d_ruo, d_rprims, d_amap, nullptr, nullptr, (int)nb, map_off, ps,
+                                                             nullptr, nullptr, d_src);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
 }

@@ -145,6 +145,7 @@ class ShaderSpec:
     attributes: torch.Tensor | None = None  # int32[V, words]
     vertex_count: int = 0
     batch_vertex_base: torch.Tensor | None = None  # int32[n_batches]: multi-draw (draws.py)
+    extra_cycles: int = 0  # synthetic shader load per invocation (ShaderFn.cycles - 1)
 
 
 class DeviceRun:
@@ -252,6 +253,21 @@ class DeviceRun:
         return out
 
 
+def ideal_counts(d_indices: torch.Tensor, vertex_count: int):
+    """analytics.py:105-119 on the device: (number of referenced vertices, int32[vertex_count] 0/1 flags)."""
+    lib = N.require_cuda()
+    dev = d_indices.device
+    counts = torch.empty(max(vertex_count, 1), dtype=torch.int32, device=dev)
+    out = torch.zeros(2, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        raise_status(lib.vr_ideal_counts(_ptr(d_indices), d_indices.numel(), vertex_count, _ptr(counts), _ptr(out),
+                                         _stream_ptr()))
+    referenced, status = (int(v) for v in out.cpu().numpy())
+    if status:
+        raise_status(status)
+    return referenced, counts[:vertex_count]
+
+
 class RunBuffers:
     """Reusable output + workspace allocation for repeated runs of one shape (bench, serving)."""
 
@@ -311,6 +327,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
     sh = N.ShaderC()
     sh.kind = shader.kind
     sh.vertex_count = shader.vertex_count
+    sh.extra_cycles = int(shader.extra_cycles)
     if shader.batch_vertex_base is not None:
         sh.d_batch_vertex_base = shader.batch_vertex_base.data_ptr()
     if shader.kind == N.VR_SHADER_POSITION:

@@ -298,8 +298,11 @@ def _shader_spec(shader: ShaderFn, device, vertex_count):
     if cache is None or cache.device != device:
         cache = engine.to_device_positions4(mesh.positions, device)
         object.__setattr__(mesh, "_vr_pos4", cache)
+    # ShaderFn.cycles (strategies.py:40-44) is the abstract per-invocation load of the cost model; on the device
+    # cycles > 1 runs that many extra dependent FMAs per invocation (PAPER.md:661's synthetic shader loads)
     return engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=cache, matrix=matrix,
-                             vertex_count=vertex_count or mesh.vertex_count), True
+                             vertex_count=vertex_count or mesh.vertex_count,
+                             extra_cycles=max(int(shader.cycles) - 1, 0)), True
 
 
 def run_on_indices(strategy: str, indices, batches, cfg: BatchConfig, shader: ShaderFn,

@@ -11,6 +11,8 @@ Writes, next to this file:
                 identity + position shader, per-vertex tallies, streams)
   dynamic.npz   dynamic_batches offsets on meshes / random buffers
   grid256.json  the config-1/2 table of BASELINE.md (gen_grid(256,256))
+  walk.npz      random-walk client: likelihood tables, uniforms, trajectories and reports (walk.py)
+  cache.json    simulate_parallel_cache / ideal_report results on small meshes (cache.py, analytics.py)
 The files are committed; the GPU box never sees /root/reference.
 """
 from __future__ import annotations
@@ -167,6 +169,67 @@ def make_dynamic():
     print("dynamic:", k, "cases")
 
 
+def make_walk():
+    from vrlab import walk as W
+    out = {}
+    cfgs = {
+        "default_small": W.WalkConfig(grid=(48, 40), agents=700, max_move_distance=5, kept_moves=4, steps=4, rng_seed=3),
+        "radius16": W.WalkConfig(grid=(64, 64), agents=300, steps=2, rng_seed=11),
+        "uniform_field": W.WalkConfig(grid=(30, 30), agents=200, max_move_distance=3, kept_moves=6, gaussians=(), steps=3,
+                                      rng_seed=5),
+        "one_peak": W.WalkConfig(grid=(40, 56), agents=500, max_move_distance=7, kept_moves=8, steps=3, rng_seed=9,
+                                 gaussians=(W.Gaussian(center=(10.5, 30.25), sigma=4.0, amplitude=2.0),)),
+    }
+    for name, cfg in cfgs.items():
+        out[f"{name}/cfg"] = np.array([cfg.grid[0], cfg.grid[1], cfg.agents, cfg.max_move_distance, cfg.kept_moves,
+                                       cfg.steps, cfg.rng_seed], dtype=np.int64)
+        out[f"{name}/gaussians"] = np.array([[g.center[0], g.center[1], g.sigma, g.amplitude] for g in cfg.gaussians],
+                                            dtype=np.float64).reshape(-1, 4)
+        rng = np.random.default_rng(1)
+        cells = np.array([W.pack_cell(int(rng.integers(0, cfg.grid[0])), int(rng.integers(0, cfg.grid[1])))
+                          for _ in range(40)] + [W.pack_cell(0, 0), W.pack_cell(cfg.grid[0] - 1, cfg.grid[1] - 1),
+                                                 W.pack_cell(0, cfg.grid[1] - 1)], dtype=np.uint32)
+        out[f"{name}/cells"] = cells
+        out[f"{name}/tables"] = np.stack([W.cell_likelihoods(int(c), cfg) for c in cells])
+        out[f"{name}/uniforms"] = np.stack([W.agent_uniforms(cfg.rng_seed, t, np.arange(cfg.agents)) for t in range(3)])
+        traj = W.naive_walk(cfg)
+        out[f"{name}/trajectory"] = traj
+        for strategy in ("sort", "hash", "warp", "naive", "phash"):
+            bcfg = BatchConfig(primitive_size=1, batch_size=96 if strategy in ("warp", "naive") else 576)
+            run = W.run_walk(cfg, strategy, bcfg)
+            assert np.array_equal(run.trajectory, traj), (name, strategy)
+            out[f"{name}/{strategy}/reports"] = np.array(
+                [[r.indices, r.invocations, r.batches,
+                  r.probe_stats.fast if r.probe_stats else -1, r.probe_stats.slow if r.probe_stats else -1,
+                  r.probe_stats.max_chain if r.probe_stats else -1] for r in run.reports], dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "walk.npz"), **out)
+    print("walk.npz:", len(out), "arrays")
+
+
+def make_cache():
+    from vrlab.analytics import ideal_report
+    from vrlab.cache import CacheConfig, ideal_reuse, simulate_parallel_cache
+    from vrlab.mesh import gen_grid, gen_icosphere, shuffle_triangles
+    meshes = {"grid40x31": gen_grid(40, 31), "grid40x31s": shuffle_triangles(gen_grid(40, 31), 4),
+              "sphere3": gen_icosphere(3), "grid9x9": gen_grid(9, 9)}
+    cases = []
+    for mname, mesh in meshes.items():
+        ir = ideal_report(mesh)
+        for (procs, wave, entries) in [(28, 1024, 256), (4, 32, 16), (1, 1, 10 ** 6), (3, 96, 64), (7, 8, 5),
+                                       (2, 3, 1), (1, 64, 48), (5, 1024, 8)]:
+            miss = np.zeros(mesh.vertex_count, dtype=np.int64)
+            rep = simulate_parallel_cache(mesh.indices, CacheConfig(num_processors=procs, wave_width=wave, entries=entries),
+                                          miss_counts=miss)
+            cases.append(dict(mesh=mname, procs=procs, wave=wave, entries=entries, hits=rep.hits, misses=rep.misses,
+                              hit_rate=rep.hit_rate, miss_counts_sum=int(miss.sum()),
+                              miss_counts_crc=int((miss * (np.arange(len(miss)) % 9973 + 1)).sum())))
+        cases.append(dict(mesh=mname, ideal_invocations=ir.invocations, ideal_reuse=ideal_reuse(mesh.indices),
+                          ideal_rate=ir.reuse_rate))
+    with open(os.path.join(HERE, "cache.json"), "w") as fh:
+        json.dump(cases, fh, indent=1)
+    print("cache.json:", len(cases), "cases")
+
+
 def next_pow2(x):
     p = 1
     while p < x:
@@ -201,7 +264,8 @@ def make_grid256():
 
 
 if __name__ == "__main__":
-    make_kernels()
-    make_dynamic()
-    make_runs()
-    make_grid256()
+    only = sys.argv[1:]
+    for name, fn in (("kernels", make_kernels), ("dynamic", make_dynamic), ("runs", make_runs),
+                     ("grid256", make_grid256), ("walk", make_walk), ("cache", make_cache)):
+        if not only or name in only:
+            fn()
