@@ -433,12 +433,15 @@ def main():
         alg = algorithmic_bytes(n_idx, inv, nb)
         launches = lib.vr_last_launch_count()
         path = lib.vr_last_kernel_path()
-        fused = path >= 2  # init + one kernel that dedups, places and shades
+        fused = path in (2, 3)  # init + one kernel that dedups, places and shades (4 = the three-kernel sort/hash path)
         dom = int(np.argmax(stage_ms))
         # per-kernel algorithmic bytes: dedup = index read + map write + metadata;
         # shade/finalize = staged id read is not algorithmic: position read + shaded write
         kernel_alg = {"dedup": 4 * n_idx + 2 * n_idx + 12 * nb, "shade_finalize": 32 * inv}
         dom_name = (N.KERNEL_PATH_NAMES.get(path) if fused else None) or N.PROFILE_STAGE_NAMES[dom]
+        if path == 4:  # vr_dyn3.cuh: A (+ B) are timed as 'dedup', C as 'shade_finalize'
+            dom_name = {"dedup": "dyn3 A: set dedup + look-back offsets (+ B: table replay)",
+                        "shade_finalize": "dyn3 C: ranks + local indices + shading"}.get(N.PROFILE_STAGE_NAMES[dom], dom_name)
         traffic = None  # DRAM bytes per step of the dominant kernel, from the committed ncu --set full capture
         for tf in ("r2_traffic.json", "r1_traffic.json"):
             try:
@@ -691,6 +694,66 @@ def main():
             res["incl_redundant_boundary_scan"] = {"ms_per_step": ms_w, "value": tris / (ms_w * 1e-3)}
         return res
 
+    def run_shader_load(steps, warmup):
+        """PAPER.md:661 / :696-714: where reuse pays.  The stage on the configs[2] mesh with a synthetic shader load of
+        0 / 256 / 1024 dependent FMAs per invocation: no reuse (naive, 3 invocations per triangle) against static
+        warp-voting batches and dynamic sort batches."""
+        wl = WORKLOADS["c3_warp"]
+        mesh = build_mesh(wl)
+        cfg = P.BatchConfig()
+        hcfg = HashConfig(table_size=cfg.block_size)
+        n_idx = len(mesh.indices)
+        d_idx = engine.to_device_indices(mesh.indices, dev)
+        pos4 = engine.to_device_positions4(mesh.positions, dev)
+        stat = engine.static_offsets_device(n_idx, cfg, dev)
+        dyn = engine.dynamic_offsets_device(d_idx, cfg)
+        out = {}
+        for cycles in (0, 256, 1024):
+            spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=pos4, matrix=MATRIX,
+                                     vertex_count=mesh.vertex_count, extra_cycles=cycles)
+            row = {}
+            for strat, offs, static in (("naive", stat, True), ("warp", stat, True), ("sort", dyn, False)):
+                nb = offs.numel() - 1
+                plan = engine.run_device(strat, d_idx, offs[:-1], offs[1:], nb, n_idx,
+                                         cfg.batch_size if static else max(cfg.batch_size, cfg.max_indices), cfg, hcfg, spec,
+                                         buffers=engine.RunBuffers(), static=static, plan_only=True)
+                for _ in range(warmup):
+                    run = plan.relaunch()
+                run.check()
+                ms = timed_steps(plan.relaunch, steps)[0] / steps
+                row[strat] = {"ms_per_step": ms, "value": mesh.triangle_count / (ms * 1e-3), "invocations": run.invocations}
+            row["speedup_warp_vs_naive"] = row["naive"]["ms_per_step"] / row["warp"]["ms_per_step"]
+            row["speedup_sort_vs_naive"] = row["naive"]["ms_per_step"] / row["sort"]["ms_per_step"]
+            out[f"cycles_{cycles}"] = row
+        return out
+
+    def run_clients(steps):
+        """SURVEY.md 8f rows on the device: ideal counts and the LRU cache model on the configs[2] mesh, one step of the
+        random-walk client (walk.py defaults: 300 000 agents, 256 x 256 grid, radius 16, 8 moves kept)."""
+        from paper_1805_08893_b200 import walk as W
+        mesh = build_mesh(WORKLOADS["c3_warp"])
+        d_idx = engine.to_device_indices(mesh.indices, dev)
+        out = {}
+        ms = timed_steps(lambda: engine.ideal_counts(d_idx, mesh.vertex_count), 5)[0] / 5
+        referenced, _ = engine.ideal_counts(d_idx, mesh.vertex_count)
+        out["ideal_report"] = {"ms": ms, "invocations": referenced, "reuse_rate": 1 - referenced / len(mesh.indices)}
+        t0 = time.perf_counter()
+        rep = P.simulate_parallel_cache(d_idx, P.CacheConfig())
+        out["lru_cache_28x1024x256"] = {"wall_s": time.perf_counter() - t0, "hit_rate": rep.hit_rate, "misses": rep.misses}
+        wcfg = W.WalkConfig(steps=1)
+        pos = W._to_device_positions(W.initial_positions(wcfg))
+        bcfg = P.BatchConfig(primitive_size=1, batch_size=576)
+        for strat in ("sort", "hash"):
+            W._step_device(pos, wcfg, 0, strat, bcfg, None, "walk")  # warm-up
+            t = timed_steps(lambda: W._step_device(pos, wcfg, 0, strat, bcfg, None, "walk"), 5)[0] / 5
+            _, rep = W._step_device(pos, wcfg, 0, strat, bcfg, None, "walk")
+            out[f"walk_step_{strat}"] = {"ms": t, "agents": wcfg.agents, "evaluations": rep.invocations,
+                                         "reuse_rate": rep.reuse_rate, "agents_per_s": wcfg.agents / (t * 1e-3)}
+        d_cells = W._pack_device(pos)
+        t = timed_steps(lambda: W._likelihoods_device(d_cells, wcfg), 3)[0] / 3
+        out["walk_step_no_reuse_likelihoods_ms"] = t
+        return out
+
     res, e2e = run_workload(args.workload, args.steps, args.warmup, True)
     others = {}
     if not args.no_others:
@@ -700,6 +763,9 @@ def main():
                 others[name] = run_workload(name, o_steps, args.warmup, False)[0]
         for strat in ("sort", "hash"):
             others[f"c5_multidraw_{strat}"] = run_multidraw(strat, o_steps, args.warmup)
+        if world == 1:
+            others["shader_load"] = run_shader_load(max(5, min(args.steps, 10)), args.warmup)
+            others["clients"] = run_clients(5)
     sharded = {}
     if world > 1 or args.sharded:
         s_steps = max(10, min(args.steps, 20))

@@ -50,7 +50,6 @@ struct DebugKnobs {
     int rows_lag = 0;         // VR_LAG           tile kernel: shade lag in tiles (0 = 1.5 x resident CTAs)
     int no_pdl = 0;           // VR_NO_PDL        no programmatic dependent launch
     int dyn3_prefetch = 0;    // VR_DYN3_PREFETCH three-kernel path: L2 prefetch of the distinct vertices before the sort
-    int dyn_single = 0;       // VR_DYN_SINGLE    batch formation: (reserved)
 };
 inline const DebugKnobs& debug_knobs() {
     static const DebugKnobs k = [] {
@@ -60,7 +59,7 @@ inline const DebugKnobs& debug_knobs() {
         geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run);
         flag("VR_GREEDY_GLOBAL", d.greedy_global); flag("VR_WALK_GLOBAL", d.walk_global); flag("VR_SORT_CTA", d.sort_cta);
         geti("VR_PREFETCH", d.rows_prefetch); geti("VR_LAG", d.rows_lag); flag("VR_NO_PDL", d.no_pdl);
-        geti("VR_DYN3_PREFETCH", d.dyn3_prefetch); geti("VR_DYN_SINGLE", d.dyn_single);
+        geti("VR_DYN3_PREFETCH", d.dyn3_prefetch);
         return d;
     }();
     return k;
