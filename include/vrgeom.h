@@ -14,7 +14,9 @@
  *     never frees caller memory and keeps no state between calls;
  *   - every call is asynchronous on `stream` (a cudaStream_t passed as void*);
  *     results are valid after the caller synchronises that stream;
- *   - calls are re-entrant across streams as long as outputs/workspaces differ;
+ *   - calls are re-entrant across streams and host threads as long as outputs/workspaces differ (the only
+ *     library state is the per-thread diagnostics of vr_profile_* / vr_last_*, and debugging knobs read from
+ *     the environment once per process);
  *   - functions return a vr_status; host-detectable misuse is reported
  *     immediately, data-dependent violations (found by the kernels) are reported
  *     through vr_stats.error_code / error_batch, read back by the caller;
@@ -277,16 +279,18 @@ int vr_walk_pack(const int32_t *d_positions, int64_t n_agents, uint32_t *d_cells
 
 /* Profiling aid (bench.py): per-kernel device time of the last vr_run, measured with CUDA
  * events on the launching stream.  Stages, in order: init (+ span scan), dedup, offset scan
- * (+ statistics), shade/finalize.  Process-wide; do not enable under concurrent vr_run calls.
+ * (+ statistics), shade/finalize (the three-kernel sort/hash path reports its kernels A (+ B) as "dedup" and C as
+ * "shade/finalize").  State is per host THREAD: a thread reads what its own last vr_run recorded.
  * vr_profile_read synchronises the last event and returns the number of stages written. */
 #define VR_PROFILE_STAGES 4
 int vr_profile_enable(int on);
-/* Number of kernels the last vr_run of this process launched (bench.py's gpu_launches). */
+/* Number of kernels the calling thread's last vr_run launched (bench.py's gpu_launches). */
 int vr_last_launch_count(void);
 int vr_profile_read(float *ms, int cap);
-/* Which dedup path the last vr_run of this process took (tests and bench.py report it):
+/* Which dedup path the calling thread's last vr_run took (tests and bench.py report it):
  * 0 = generic kernels (K1 -> K2 -> K3), 1 = static-batch warp kernel (unfused), 2 = static-batch warp
- * kernel with fused look-back + shading, 3 = persistent tile kernel (csrc/vr_warp_rows.cuh). */
+ * kernel with fused look-back + shading, 3 = persistent tile kernel (csrc/vr_warp_rows.cuh), 4 = three-kernel
+ * sort / hash / phash path for budgeted batches (csrc/vr_dyn3.cuh). */
 int vr_last_kernel_path(void);
 
 #ifdef __cplusplus

@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                     if (idx >= 0) word = ld_relaxed_gpu_u64(state + idx);
                     if (__all_sync(0xffffffffu, (word >> 62) != 0)) break;
                     __nanosleep(64);  // the predecessors are busy deduplicating: leave them the issue slots
-                    if (++spins > (1 << 22)) { lost = true; break; }
+                    if (++spins > (1 << 12)) __nanosleep(500);  // (a preempted producer is not a lost one: ~0.5 s before giving up)
+                    if (spins > (1 << 20)) { lost = true; break; }
                 }
                 if (lost) break;
                 const uint32_t incl = __ballot_sync(0xffffffffu, (word >> 62) == 2);

@@ -1717,12 +1717,13 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
 }
 
 // Optional per-kernel timing of the last vr_run (a profiling aid for bench.py: CUDA events on
-// the launching stream between the pipeline's kernels).  Process-wide state: while enabled,
-// vr_run is not re-entrant.
-static cudaEvent_t g_prof_ev[VR_PROFILE_STAGES + 1];
-static int g_prof_on = 0, g_prof_marks = 0;
-static int g_last_launches = 0;  // kernels launched by the last vr_run of this process
-static int g_last_path = 0;      // see vr_last_kernel_path()
+// the launching stream between the pipeline's kernels).  Per host thread, like the two "last run" values
+// below: vr_run itself keeps no state, so concurrent callers on different threads / streams do not disturb
+// each other's diagnostics.
+static thread_local cudaEvent_t g_prof_ev[VR_PROFILE_STAGES + 1];
+static thread_local int g_prof_on = 0, g_prof_marks = 0;
+static thread_local int g_last_launches = 0;  // kernels launched by this thread's last vr_run
+static thread_local int g_last_path = 0;      // see vr_last_kernel_path()
 static inline void prof_mark(cudaStream_t s) {
     if (g_prof_on && g_prof_marks <= VR_PROFILE_STAGES) cudaEventRecord(g_prof_ev[g_prof_marks++], s);
 }

@@ -153,7 +153,11 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
         for (;;) {
             mine = ld_acquire_gpu_u64(c.tile_state + stile);  // every thread acquires: the scratch is visible to it
             if (__all_sync(0xffffffffu, (mine >> 62) != 0)) break;
-            if (++spins > (1 << 22)) { lost = true; break; }
+            // (forward progress is guaranteed by ticket order; the bound only turns a broken launch into an error
+            // instead of a hang, and backs off so that a preempted / time-sliced producer is not mistaken for one:
+            // 2^12 polls at full rate, then ~2^20 x 0.5 us)
+            if (++spins > (1 << 12)) __nanosleep(500);
+            if (spins > (1 << 20) + (1 << 12)) { lost = true; break; }
         }
     }
     VR_MARK(8);
@@ -226,7 +230,8 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
                     pending |= !found && (word[k] >> 62) == 0 && (sum[k] >> 58) != (unsigned long long)kRowGroup;
                 }
                 if (!__any_sync(0xffffffffu, pending)) break;
-                if (++spins > (1 << 22)) { lost = true; break; }
+                if (++spins > (1 << 12)) __nanosleep(500);
+                if (spins > (1 << 20) + (1 << 12)) { lost = true; break; }
             }
             if (lost) break;
             if (first && lane < pos) {
