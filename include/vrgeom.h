@@ -220,6 +220,10 @@ int vr_expand_stream(const int32_t *d_batch_round_off, const int32_t *d_round_ui
                      float *d_stream_pos3, uint32_t *d_stream_ids, void *d_workspace,
                      size_t workspace_bytes, void *stream);
 
+/* strategies.py:53-67 records are float32[3] (x/w, y/w, z/w); the stage keeps float4 (+ w) for 16-byte stores.
+ * Packs d_shaded4[n] to float[3*n] -- what a caller copies to the host when it wants the reference's record. */
+int vr_pack_xyz(const float *d_shaded4, int64_t n, float *d_xyz, void *stream);
+
 /* Same walk as vr_expand_stream, but out[slot] = round base + assembly_map[slot]: the position of the
  * slot's record in the unique-id / shaded arrays (int32[n_slots]).  Clients that attach their own
  * per-unique payload (the random-walk client below) expand it with this. */

@@ -1663,6 +1663,24 @@ __global__ void __launch_bounds__(256) batch_vertex_base_kernel(const int32_t* _
     out[b] = draw_vbase[lo];
 }
 
+// float4 (x/w, y/w, z/w, w) -> the reference's float32[3] record: 4 records in, 3 x 16 bytes out per thread
+__global__ void __launch_bounds__(256) pack_xyz_kernel(const float4* __restrict__ in, int64_t n, float* __restrict__ out) {
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // group of 4 records
+    const int64_t i = 4 * q;
+    if (i + 4 <= n) {
+        const float4 a = in[i], b = in[i + 1], c4 = in[i + 2], d = in[i + 3];
+        float4* o = reinterpret_cast<float4*>(out + 3 * i);
+        o[0] = make_float4(a.x, a.y, a.z, b.x);
+        o[1] = make_float4(b.y, b.z, c4.x, c4.y);
+        o[2] = make_float4(c4.z, d.x, d.y, d.z);
+    } else {
+        for (int64_t k = i; k < n; k++) {
+            const float4 v = in[k];
+            out[3 * k] = v.x; out[3 * k + 1] = v.y; out[3 * k + 2] = v.z;
+        }
+    }
+}
+
 __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __restrict__ off) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nb) off[i] = (int32_t)(i * bs);
@@ -2152,6 +2170,16 @@ int vr_expand_stream(const int32_t* d_bro, const int32_t* d_ruo, const int32_t* 
     span_only_scan_kernel<<<1, 1024, 0, stream>>>(d_bbegin, d_bend, (int)nb, map_off);
     expand_kernel<<<(int)ceil_div(nb, 8), 256, 0, stream>>>(d_bro, d_ruo, d_rprims, d_amap, d_uids,
                                                              (const float4*)d_shaded4, (int)nb, map_off, ps, d_pos3, d_ids, nullptr);
+    VR_CUDA_CHECK(cudaGetLastError());
+    return VR_OK;
+}
+
+int vr_pack_xyz(const float* d_shaded4, int64_t n, float* d_xyz, void* stream) {
+    if (n < 0) return VR_ERR_BAD_CONFIG;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (n == 0) return VR_OK;
+    if (!d_shaded4 || !d_xyz || ((uintptr_t)d_xyz & 15) || ((uintptr_t)d_shaded4 & 15)) return VR_ERR_BAD_CONFIG;
+    pack_xyz_kernel<<<(int)ceil_div(ceil_div(n, 4), 256), 256, 0, (cudaStream_t)stream>>>((const float4*)d_shaded4, n, d_xyz);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
 }

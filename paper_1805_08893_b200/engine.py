@@ -230,6 +230,17 @@ class DeviceRun:
             out["shade_counts"] = self.shade_counts.cpu().numpy().astype(np.int64)
         return out
 
+    def shaded_xyz(self, count: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """The shaded records in the reference's layout, float32[count, 3] (strategies.py:53-67), packed on the device
+        (vr_pack_xyz): what crosses PCIe when the host wants the records."""
+        lib = N.require_cuda()
+        n = self.invocations if count is None else count
+        if out is None:
+            out = torch.empty((n, 3), dtype=torch.float32, device=self.stats_dev.device)
+        with torch.cuda.device(self.stats_dev.device):
+            raise_status(lib.vr_pack_xyz(_ptr(self.shaded4), n, _ptr(out), _stream_ptr()))
+        return out[:n]
+
     def expand_stream(self, positions: bool):
         """Per-corner record stream (strategies.py:456-463) built on the device."""
         self.check()

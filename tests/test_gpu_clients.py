@@ -126,3 +126,14 @@ def test_synthetic_shader_load_leaves_results_unchanged(cuda_lib, strategy):
     assert np.array_equal(base[0].device_run.flat()["shaded"], loaded[0].device_run.flat()["shaded"])
     cost = P.estimate_cost(loaded[1], P.position_shader(mesh, MATRIX, cycles=513))
     assert cost.total_cycles == 513 * loaded[1].invocations
+
+
+def test_pack_xyz(cuda_lib):
+    """vr_pack_xyz: the stage's float4 records as the reference's float32[3] records (strategies.py:53-67)."""
+    mesh = P.gen_grid(37, 29)
+    cfg = BatchConfig()
+    stream, _ = P.run_warp_voting(mesh, P.static_batches(len(mesh.indices), cfg), cfg, P.position_shader(mesh, MATRIX))
+    run = stream.device_run
+    for count in (run.invocations, run.invocations - 1, run.invocations - 2, run.invocations - 3, 1):
+        xyz = run.shaded_xyz(count).cpu().numpy()
+        assert xyz.shape == (count, 3) and np.array_equal(xyz, run.shaded4[:count, :3].cpu().numpy())
