@@ -674,8 +674,9 @@ def main():
     def run_sharded_stream(name, steps, warmup):
         """Strong scaling: ONE stream of the workload cut into whole batches per rank (shard.run_sharded); the
         full index stream and the vertex buffer are replicated, every rank dedups and shades its slice, the
-        statistics blocks are merged by one all-gather.  Dynamic batches: every rank runs the index-only
-        boundary scan over the whole stream (SURVEY.md 8e option (i)); reported with and without it."""
+        statistics blocks are merged by one all-gather.  Dynamic batches: reported with the offsets precomputed, and
+        including batch formation -- by the boundary exchange (every rank scans its own range, one all-gather of
+        small tables: SURVEY.md 8e option (ii)) and by the redundant whole-stream scan (option (i))."""
         wl = WORKLOADS[name]
         mesh = build_mesh(wl)
         cfg = workload_cfg(wl)
@@ -704,13 +705,16 @@ def main():
         res = {"workload": wl["desc"], "scaling": "strong", "value": tris / (ms * 1e-3), "ms_per_step": ms,
                "batches_per_rank": plan.n_batches, "frac_of_n_x_peak": alg / (ms * 1e-3) / 1e9 / (peak * world)}
         if not static:
-            def whole():
-                r, _ = shard.run_sharded(wl["strategy"], d_idx, cfg, hcfg, spec, batching="dynamic", rank=rank, world=world,
-                                         buffers=bufs)
-            whole()
             f_steps = max(5, min(steps, 20))
-            ms_w = timed_steps(whole, f_steps)[0] / f_steps
-            res["incl_redundant_boundary_scan"] = {"ms_per_step": ms_w, "value": tris / (ms_w * 1e-3)}
+            for label, mode in (("incl_boundary_exchange", "exchange"), ("incl_redundant_boundary_scan", "dynamic")):
+                # batch formation inside the step: "exchange" = every rank scans its own range, one all-gather of
+                # 2.7 KB tables (SURVEY.md 8e option (ii)); "dynamic" = every rank scans the whole stream (option (i))
+                def whole():
+                    shard.run_sharded(wl["strategy"], d_idx, cfg, hcfg, spec, batching=mode, rank=rank, world=world, buffers=bufs)
+                whole()
+                ms_w = timed_steps(whole, f_steps)[0] / f_steps
+                res[label] = {"ms_per_step": ms_w, "value": tris / (ms_w * 1e-3),
+                              "frac_of_n_x_peak": (alg + 4 * len(mesh.indices)) / (ms_w * 1e-3) / 1e9 / (peak * world)}
         return res
 
     def run_shader_load(steps, warmup):

@@ -187,6 +187,32 @@ int vr_dynamic_batches_draws(const uint32_t *d_indices, int64_t n_indices, const
                              const int32_t *d_draw_index_start, int32_t n_draws, int32_t *d_offsets,
                              int64_t *d_n_batches, void *d_workspace, size_t workspace_bytes,
                              void *stream);
+/* Batch formation over a stream that is SHARDED across GPUs (SURVEY.md 8e option (ii)).  A greedy boundary depends on
+ * all boundaries before it, so a rank cannot cut its own range of the stream on its own -- but what a range does to
+ * the chain of boundaries is a small table "offset at which the chain enters the range -> (offset at which it enters
+ * the next range, batches started inside)", cap = max_indices / primitive_size entries, and tables compose.  So:
+ *   1. every rank calls vr_dynamic_range_tables on ITS range (whole groups [group_lo, group_hi) of
+ *      vr_dynamic_group_indices() indices each; the index buffer is replicated): stage A and the chunk / group
+ *      tables for that range only, and the range's table -> d_table[vr_dynamic_table_words()];
+ *   2. ONE all-gather of the tables (2 * cap int32 per rank: 2.7 KB at the defaults) -- the path's only exchange;
+ *   3. every rank calls vr_dynamic_range_offsets with the gathered tables [world][table_words] (same workspace as
+ *      in step 1, untouched in between): its true entry offset, then the offsets of the batches that START in
+ *      its range, d_offsets[0 .. count] (positions in the whole buffer; the closing entry is the start of the next
+ *      rank's first batch, or n_indices), d_counts (device int64[4]) = {count, vr_status, global number of the
+ *      range's first batch, batches of the whole stream}.
+ * The concatenation of the ranks' offsets is exactly vr_dynamic_batches' array.  Workspace: vr_dynamic_workspace_bytes.
+ * VR_ERR_UNSUPPORTED for batch windows the default kernels do not take (fall back to a redundant whole-stream scan). */
+int64_t vr_dynamic_group_count(int64_t n_indices, const vr_batch_config *cfg);
+int64_t vr_dynamic_group_indices(const vr_batch_config *cfg);
+int64_t vr_dynamic_table_words(int64_t n_indices, const vr_batch_config *cfg);
+int vr_dynamic_range_tables(const uint32_t *d_indices, int64_t n_indices, const vr_batch_config *cfg,
+                            int64_t group_lo, int64_t group_hi, int32_t *d_table, void *d_workspace,
+                            size_t workspace_bytes, void *stream);
+int vr_dynamic_range_offsets(const uint32_t *d_indices, int64_t n_indices, const vr_batch_config *cfg,
+                             int64_t group_lo, int64_t group_hi, const int32_t *d_tables, int32_t world,
+                             int32_t rank, int32_t *d_offsets, int64_t *d_counts, void *d_workspace,
+                             size_t workspace_bytes, void *stream);
+
 /* Per-batch first vertex for vr_shader.d_batch_vertex_base: batch b lies in the draw that holds
  * d_batch_begin[b]; d_out[b] = d_draw_vertex_base[that draw] (device int32 arrays). */
 int vr_batch_vertex_base(const int32_t *d_batch_begin, int64_t n_batches, const int32_t *d_draw_index_start,

@@ -92,6 +92,13 @@ _SIGNATURES = {
                                      C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vr_dynamic_batches_draws": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(BatchConfigC), C.c_void_p, C.c_int32,
                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_dynamic_group_count": (C.c_int64, [C.c_int64, C.POINTER(BatchConfigC)]),
+    "vr_dynamic_group_indices": (C.c_int64, [C.POINTER(BatchConfigC)]),
+    "vr_dynamic_table_words": (C.c_int64, [C.c_int64, C.POINTER(BatchConfigC)]),
+    "vr_dynamic_range_tables": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(BatchConfigC), C.c_int64, C.c_int64, C.c_void_p,
+                                          C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_dynamic_range_offsets": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(BatchConfigC), C.c_int64, C.c_int64, C.c_void_p,
+                                           C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vr_batch_vertex_base": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
                                        C.c_void_p]),
     "vr_output_bounds": (C.c_int, [C.c_int, C.c_int64, C.c_int64, C.POINTER(BatchConfigC),

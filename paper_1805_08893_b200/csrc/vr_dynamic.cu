@@ -63,6 +63,13 @@ struct DynCtx {
     // crosses a draw (the reference runs dynamic_batches once per draw).  NULL = one draw.
     const int32_t* __restrict__ draw_start;
     int n_draws;
+    // a RANGE of the stream (multi-GPU, SURVEY.md 8e option (ii)): whole groups [g_lo, g_hi) = chunks [k_lo, k_hi) =
+    // start primitives [s_lo, s_hi).  The whole stream: 0 .. n_groups / n_chunks / T.
+    int g_lo, g_hi, k_lo, k_hi, s_lo, s_hi;
+    int tile_lo;            // first tile of the link kernel
+    int ranged;             // 1: offsets are written relative to the range's first batch, see vr_dynamic_range_*
+    int32_t* r_table;       // [2 * cap] out: entry offset -> (exit offset, batches) of the whole range
+    const int32_t* entry;   // [2] in (ranged): entry offset into the range, global number of its first batch
 };
 
 // (the buffer starts 256-byte aligned and is padded: whole 16-byte stores)
@@ -149,7 +156,7 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
     uint16_t* bucket = slot_of + tile + halo;                         // [tile + halo] relative positions
     __shared__ uint32_t s_part[kLinkThreads];
     const int t = threadIdx.x;
-    const int t0 = blockIdx.x * tile;
+    const int t0 = (c.tile_lo + blockIdx.x) * tile;
     const int t1 = min(c.n, t0 + tile);
     int hs = t0 - halo;
     if (hs < 0) hs = 0;
@@ -294,7 +301,7 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
     uint16_t* dp = reinterpret_cast<uint16_t*>(smem_raw);  // [npos_max] position - prev
     uint16_t* dn = dp + npos_max;                          // [npos_max] next - position
     const int ps = c.ps;
-    const int p0 = blockIdx.x * blockDim.x * run;          // first start primitive of the CTA
+    const int p0 = c.s_lo + blockIdx.x * blockDim.x * run;  // first start primitive of the CTA
     const int base = ps * p0;
     const int npos = min(c.n - base, npos_max);
     auto put = [&](int r, int pv, int nx) {
@@ -317,8 +324,8 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
     }
     __syncthreads();
     const int s0 = p0 + threadIdx.x * run;
-    if (s0 >= c.T) return;
-    const int s1 = min(c.T, s0 + run);
+    if (s0 >= c.s_hi) return;
+    const int s1 = min(c.s_hi, s0 + run);
     int e = s0, cnt = 0;
     int d = 0, dend = c.T;
     if (c.draw_start) {
@@ -367,7 +374,7 @@ __global__ void draws_check_kernel(DynCtx c) {
 
 // ---- B1: chunk tables ---------------------------------------------------------------------
 __global__ void __launch_bounds__(256) chunk_table_kernel(DynCtx c) {
-    const int k = blockIdx.x;
+    const int k = c.k_lo + blockIdx.x;
     const int lo = k * c.chunk, hi = min(c.T, lo + c.chunk);
     for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
         int s = lo + o, cnt = 0;
@@ -380,7 +387,7 @@ __global__ void __launch_bounds__(256) chunk_table_kernel(DynCtx c) {
 
 // ---- B2: group tables (compose kGroup chunk tables for every entry offset) -----------------
 __global__ void __launch_bounds__(256) group_table_kernel(DynCtx c) {
-    const int g = blockIdx.x;
+    const int g = c.g_lo + blockIdx.x;
     const int k0 = g * kGroup, k1 = min(c.n_chunks, k0 + kGroup);
     for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
         int e = o, cnt = 0;
@@ -392,6 +399,33 @@ __global__ void __launch_bounds__(256) group_table_kernel(DynCtx c) {
         c.g_exit[(size_t)g * c.cap + o] = e;
         c.g_cnt[(size_t)g * c.cap + o] = cnt;
     }
+}
+
+// ---- ranges (multi-GPU): the range's own table = its group tables composed, for every entry offset ----
+__global__ void __launch_bounds__(256) range_table_kernel(DynCtx c) {
+    for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < c.cap; o += gridDim.x * blockDim.x) {
+        int e = o, cnt = 0;
+        for (int g = c.g_lo; g < c.g_hi; g++) {
+            const size_t at = (size_t)g * c.cap + e;
+            cnt += c.g_cnt[at];
+            e = c.g_exit[at];
+        }
+        c.r_table[o] = e;
+        c.r_table[c.cap + o] = cnt;
+    }
+}
+// ... and the entry of range `rank` from the tables of all ranges (gathered): the chain enters range 0 at offset
+// 0; out[0] = entry offset into range `rank`, out[1] = number of its first batch, out[2] = batches of the stream
+__global__ void range_entry_kernel(const int32_t* __restrict__ tables, int world, int rank, int cap, int32_t* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int e = 0, base = 0;
+    for (int q = 0; q < world; q++) {
+        if (q == rank) { out[0] = e; out[1] = base; }
+        const int32_t* t = tables + (size_t)q * 2 * cap;
+        base += t[cap + e];
+        e = t[e];
+    }
+    out[2] = base;
 }
 
 // ---- B3: scan over groups (one thread; n_groups is T / (chunk * kGroup)) --------------------
@@ -425,11 +459,12 @@ __global__ void __launch_bounds__(1024) table_walk_kernel(DynCtx c, int level, i
     const int* __restrict__ t_exit = level == 0 ? c.g_exit : c.c_exit;
     const int* __restrict__ t_cnt = level == 0 ? c.g_cnt : c.c_cnt;
     int k0, k1;
-    if (level == 0) { k0 = 0; k1 = c.n_groups; }
-    else { k0 = blockIdx.x * kGroup; k1 = min(c.n_chunks, k0 + kGroup); }
+    const int grp = c.g_lo + blockIdx.x;  // level 1
+    if (level == 0) { k0 = c.g_lo; k1 = c.g_hi; }
+    else { k0 = grp * kGroup; k1 = min(c.n_chunks, k0 + kGroup); }
     if (threadIdx.x == 0) {
-        s_e = level == 0 ? 0 : c.g_entry[blockIdx.x];
-        s_base = level == 0 ? 0 : c.g_base[blockIdx.x];
+        s_e = level == 0 ? (c.ranged ? c.entry[0] : 0) : c.g_entry[grp];
+        s_base = level == 0 ? (c.ranged ? c.entry[1] : 0) : c.g_base[grp];
     }
     for (int kb = k0; kb < k1; kb += rows) {
         const int nr = min(rows, k1 - kb);
@@ -455,11 +490,20 @@ __global__ void __launch_bounds__(1024) table_walk_kernel(DynCtx c, int level, i
         __syncthreads();
     }
     if (level == 0 && threadIdx.x == 0) {
-        c.g_entry[c.n_groups] = s_e;
-        c.g_base[c.n_groups] = s_base;
-        c.n_batches[0] = s_base;
-        c.n_batches[1] = 0;
-        c.offsets[s_base] = c.n;  // batching.py:124,136: last entry = end of the final batch
+        c.g_entry[c.g_hi] = s_e;
+        c.g_base[c.g_hi] = s_base;
+        if (!c.ranged) {
+            c.n_batches[0] = s_base;
+            c.n_batches[1] = 0;
+            c.offsets[s_base] = c.n;  // batching.py:124,136: last entry = end of the final batch
+        } else {  // the range's own batches, numbered from 0; the closing entry is where the chain leaves the range
+            const int local = s_base - c.entry[1];
+            c.n_batches[0] = local;
+            c.n_batches[1] = 0;
+            c.n_batches[2] = c.entry[1];
+            c.n_batches[3] = c.entry[2];
+            c.offsets[local] = (int32_t)min((long long)c.n, (long long)(c.s_hi + s_e) * c.ps);
+        }
     }
 }
 
@@ -480,10 +524,10 @@ __global__ void __launch_bounds__(128) chunk_entry_kernel(DynCtx c) {
 
 // ---- B5: offsets ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) emit_offsets_kernel(DynCtx c) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= c.n_chunks) return;
+    const int k = c.k_lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= c.k_hi) return;
     const int lo = k * c.chunk, hi = min(c.T, lo + c.chunk);
-    int s = lo + c.c_entry[k], j = c.c_base[k];
+    int s = lo + c.c_entry[k], j = c.c_base[k] - (c.ranged ? c.entry[1] : 0);
     while (s < hi) {
         c.offsets[j++] = s * c.ps;
         s = c.next[s];
@@ -493,7 +537,7 @@ __global__ void __launch_bounds__(128) emit_offsets_kernel(DynCtx c) {
 static inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct DynLayout {
-    size_t prev, nxt, next, c_exit, c_cnt, g_exit, g_cnt, g_entry, g_base, c_entry, c_base, total;
+    size_t prev, nxt, next, c_exit, c_cnt, g_exit, g_cnt, g_entry, g_base, c_entry, c_base, r_entry, total;
     int T, cap, chunk, n_chunks, n_groups, tile, slots, window;
 };
 
@@ -527,6 +571,7 @@ static DynLayout dyn_layout(int64_t n, const vr_batch_config* cfg) {
     L.g_base = o; o += al((size_t)(L.n_groups + 1) * 4);
     L.c_entry = o; o += al((size_t)L.n_chunks * 4);
     L.c_base = o; o += al((size_t)L.n_chunks * 4);
+    L.r_entry = o; o += al(16);
     L.total = o;
     return L;
 }
@@ -547,22 +592,14 @@ int vr_dynamic_batches(const uint32_t* d_idx, int64_t n, const vr_batch_config* 
     return vr_dynamic_batches_draws(d_idx, n, cfg, nullptr, 0, d_offsets, d_n_batches, d_ws, ws_bytes, stream_);
 }
 
-int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg,
-                             const int32_t* d_draw_index_start, int32_t n_draws, int32_t* d_offsets,
-                             int64_t* d_n_batches, void* d_ws, size_t ws_bytes, void* stream_) {
-    if (d_draw_index_start && n_draws <= 0) return VR_ERR_BAD_BATCH;
-    int st = vr_check_batch_config(cfg);
-    if (st) return st;
-    if (n % cfg->primitive_size != 0) return VR_ERR_UNALIGNED;  // batching.py:96-97
-    if (n < 0 || n > 0x7fffffffLL) return VR_ERR_UNSUPPORTED;
-    if (vr_device_count() == 0) return VR_ERR_CUDA;
-    cudaStream_t stream = (cudaStream_t)stream_;
-    if (n == 0) {  // batching.py:99-100
-        VR_CUDA_CHECK(cudaMemsetAsync(d_n_batches, 0, 16, stream));
-        return VR_OK;
-    }
+// mode 0: the whole stream in one call; mode 1: tables of the range [g_lo, g_hi) (stage A, B1, B2 and the range's
+// own table); mode 2: offsets of the range, given the tables of all ranges (range entry, B3 .. B5 on the range)
+static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg, const int32_t* d_draw_index_start,
+                      int32_t n_draws, int g_lo, int g_hi, int32_t* d_table, const int32_t* d_tables, int world, int rank,
+                      int32_t* d_offsets, int64_t* d_n_batches, void* d_ws, size_t ws_bytes, cudaStream_t stream) {
     DynLayout L = dyn_layout(n, cfg);
     if (!d_ws || ws_bytes < L.total) return VR_ERR_WORKSPACE;
+    if (mode != 0 && (g_lo < 0 || g_hi < g_lo || g_hi > L.n_groups)) return VR_ERR_BAD_CONFIG;
     // link table: 4-byte key + last position of the id relative to the halo start (16 bits when the
     // tile and its halo span fewer than 65 536 positions)
     const bool small_last = (int64_t)L.tile + L.window + 64 < 65536;
@@ -583,54 +620,133 @@ int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_co
     c.c_entry = (int32_t*)(ws + L.c_entry); c.c_base = (int32_t*)(ws + L.c_base);
     c.offsets = d_offsets; c.n_batches = d_n_batches;
     c.draw_start = d_draw_index_start; c.n_draws = d_draw_index_start ? n_draws : 0;
-
-    fill_kernel<<<(int)ceil_div(ceil_div(n, 4), 256), 256, 0, stream>>>(c.nxt, (int)n, kNoLink);
-    const int n_tiles = (int)ceil_div(n, L.tile);
-    // tile version: thread per position, counting sort by table slot (16-bit relative positions)
-    const int halo2 = (L.window + 31) & ~31;
+    c.ranged = mode != 0;
+    c.g_lo = mode ? g_lo : 0; c.g_hi = mode ? g_hi : L.n_groups;
+    c.k_lo = c.g_lo * kGroup; c.k_hi = (int)(c.g_hi * (int64_t)kGroup < L.n_chunks ? c.g_hi * kGroup : L.n_chunks);
+    c.s_lo = (int)((int64_t)c.k_lo * L.chunk < L.T ? (int64_t)c.k_lo * L.chunk : L.T);
+    c.s_hi = (int)((int64_t)c.k_hi * L.chunk < L.T ? (int64_t)c.k_hi * L.chunk : L.T);
+    c.r_table = d_table;
+    c.entry = (const int32_t*)(ws + L.r_entry);
     const DebugKnobs& knobs = debug_knobs();
+    const int halo2 = (L.window + 31) & ~31;
     const int tile2 = knobs.link_tile;  // (4096 / 6144: fewer CTAs per SM, measured slower)
     const int np2 = tile2 + halo2;
     const int nslots2 = (int)next_pow2((uint32_t)(np2 + np2 / 3));  // load <= 0.75
     const size_t smem2 = (size_t)nslots2 * 4 + (size_t)(nslots2 + 1) * 4 + (size_t)np2 * 4 + 16;
-    if (np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !knobs.links_warp) {
-        VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-        occurrence_links_tile_kernel<<<(int)ceil_div(n, tile2), kLinkThreads, smem2, stream>>>(c, tile2, halo2, nslots2);
-    } else if (small_last) {
-        VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        occurrence_links_kernel<uint16_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
-    } else {
-        VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        occurrence_links_kernel<int32_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
-    }
-    const int run = knobs.greedy_run;
-    const int n_threads = (int)ceil_div(L.T, run);
-    // shared-memory version when a CTA's stretch (128 runs + one batch window) fits as 16-bit distances
-    // (run * ps halfwords between the lanes' streams: an odd number of 32-bit words keeps their reads on
-    // different banks)
+    const bool links_tile = np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !knobs.links_warp;
     int run_s = 30;
     while ((run_s * c.ps) % 4 != 2 && run_s < 33) run_s++;
     const int64_t npos_s = (int64_t)128 * run_s * c.ps + L.window + c.ps;
-    if (npos_s * 4 <= 56 * 1024 && L.window < 60000 && !knobs.greedy_global) {
-        VR_CUDA_CHECK(cudaFuncSetAttribute(greedy_next_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(npos_s * 4)));
-        greedy_next_smem_kernel<<<(int)ceil_div(L.T, 128 * run_s), 128, (size_t)npos_s * 4, stream>>>(c, run_s, (int)npos_s);
-    } else {
-        greedy_next_kernel<<<(int)ceil_div(n_threads, 128), 128, 0, stream>>>(c, run);
-    }
-    chunk_table_kernel<<<L.n_chunks, 256, 0, stream>>>(c);
-    group_table_kernel<<<L.n_groups, 256, 0, stream>>>(c);
-    // B3 / B4: rows of 8 tables at a time through shared memory when they fit
+    const bool greedy_smem = npos_s * 4 <= 56 * 1024 && L.window < 60000 && !knobs.greedy_global;
     int walk_rows = 8;
     while (walk_rows > 1 && (size_t)walk_rows * L.cap * 8 > 48 * 1024) walk_rows >>= 1;
     const bool walk_smem = (size_t)walk_rows * L.cap * 8 <= 48 * 1024 && walk_rows >= 2 && !knobs.walk_global;
-    if (walk_smem) table_walk_kernel<<<1, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 0, walk_rows);
-    else group_scan_kernel<<<1, 32, 0, stream>>>(c);
-    if (c.draw_start) draws_check_kernel<<<(n_draws + 256) / 256, 256, 0, stream>>>(c);
-    if (walk_smem) table_walk_kernel<<<L.n_groups, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 1, walk_rows);
-    else chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
-    emit_offsets_kernel<<<(int)ceil_div(L.n_chunks, 128), 128, 0, stream>>>(c);
+    // (ranges are implemented by the default kernels only)
+    if (mode != 0 && (!links_tile || !greedy_smem || !walk_smem || c.draw_start)) return VR_ERR_UNSUPPORTED;
+    const int n_prims_r = c.s_hi - c.s_lo, n_chunks_r = c.k_hi - c.k_lo, n_groups_r = c.g_hi - c.g_lo;
+
+    if (mode != 2) {
+        // positions whose links are needed: the range and one batch window behind it
+        const int64_t p_lo = (int64_t)c.s_lo * c.ps;
+        const int64_t p_end = mode ? ((int64_t)c.s_hi * c.ps + L.window < n ? (int64_t)c.s_hi * c.ps + L.window : n) : n;
+        if (p_end > p_lo) fill_kernel<<<(int)ceil_div(ceil_div(p_end - p_lo, 4), 256), 256, 0, stream>>>(c.nxt + p_lo, (int)(p_end - p_lo), kNoLink);
+        const int n_tiles = (int)ceil_div(n, L.tile);
+        if (links_tile) {
+            // tile version: thread per position, counting sort by table slot (16-bit relative positions)
+            c.tile_lo = (int)(p_lo / tile2);
+            const int tiles = (int)(ceil_div(p_end, tile2) - c.tile_lo);
+            VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+            if (tiles > 0) occurrence_links_tile_kernel<<<tiles, kLinkThreads, smem2, stream>>>(c, tile2, halo2, nslots2);
+        } else if (small_last) {
+            VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            occurrence_links_kernel<uint16_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
+        } else {
+            VR_CUDA_CHECK(cudaFuncSetAttribute(occurrence_links_kernel<int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            occurrence_links_kernel<int32_t><<<(int)ceil_div(n_tiles, wpc), wpc * 32, smem, stream>>>(c, n_tiles, per_warp);
+        }
+        // shared-memory version when a CTA's stretch (128 runs + one batch window) fits as 16-bit distances
+        // (run * ps halfwords between the lanes' streams: an odd number of 32-bit words keeps their reads on
+        // different banks)
+        if (greedy_smem) {
+            VR_CUDA_CHECK(cudaFuncSetAttribute(greedy_next_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(npos_s * 4)));
+            if (n_prims_r > 0)
+                greedy_next_smem_kernel<<<(int)ceil_div(n_prims_r, 128 * run_s), 128, (size_t)npos_s * 4, stream>>>(c, run_s, (int)npos_s);
+        } else {
+            const int run = knobs.greedy_run;
+            greedy_next_kernel<<<(int)ceil_div(ceil_div(L.T, run), 128), 128, 0, stream>>>(c, run);
+        }
+        if (n_chunks_r > 0) chunk_table_kernel<<<n_chunks_r, 256, 0, stream>>>(c);
+        if (n_groups_r > 0) group_table_kernel<<<n_groups_r, 256, 0, stream>>>(c);
+        if (mode == 1) range_table_kernel<<<(int)ceil_div(L.cap, 256), 256, 0, stream>>>(c);
+    }
+    if (mode != 1) {
+        if (mode == 2) range_entry_kernel<<<1, 32, 0, stream>>>(d_tables, world, rank, L.cap, (int32_t*)(ws + L.r_entry));
+        // B3 / B4: rows of 8 tables at a time through shared memory when they fit
+        if (walk_smem) table_walk_kernel<<<1, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 0, walk_rows);
+        else group_scan_kernel<<<1, 32, 0, stream>>>(c);
+        if (c.draw_start) draws_check_kernel<<<(n_draws + 256) / 256, 256, 0, stream>>>(c);
+        if (walk_smem) { if (n_groups_r > 0) table_walk_kernel<<<n_groups_r, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 1, walk_rows); }
+        else chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
+        if (n_chunks_r > 0) emit_offsets_kernel<<<(int)ceil_div(n_chunks_r, 128), 128, 0, stream>>>(c);
+    }
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
+}
+
+int vr_dynamic_batches_draws(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg,
+                             const int32_t* d_draw_index_start, int32_t n_draws, int32_t* d_offsets,
+                             int64_t* d_n_batches, void* d_ws, size_t ws_bytes, void* stream_) {
+    if (d_draw_index_start && n_draws <= 0) return VR_ERR_BAD_BATCH;
+    int st = vr_check_batch_config(cfg);
+    if (st) return st;
+    if (n % cfg->primitive_size != 0) return VR_ERR_UNALIGNED;  // batching.py:96-97
+    if (n < 0 || n > 0x7fffffffLL) return VR_ERR_UNSUPPORTED;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    cudaStream_t stream = (cudaStream_t)stream_;
+    if (n == 0) {  // batching.py:99-100
+        VR_CUDA_CHECK(cudaMemsetAsync(d_n_batches, 0, 16, stream));
+        return VR_OK;
+    }
+    return dyn_launch(0, d_idx, n, cfg, d_draw_index_start, n_draws, 0, 0, nullptr, nullptr, 1, 0, d_offsets, d_n_batches,
+                      d_ws, ws_bytes, stream);
+}
+
+// ---- multi-GPU batch formation: ranges of whole groups, one exchange of small tables (SURVEY.md 8e option (ii)) ----
+int64_t vr_dynamic_group_count(int64_t n, const vr_batch_config* cfg) {
+    if (vr_check_batch_config(cfg) || n <= 0 || n > 0x7fffffffLL || n % cfg->primitive_size) return 0;
+    return dyn_layout(n, cfg).n_groups;
+}
+int64_t vr_dynamic_group_indices(const vr_batch_config* cfg) {
+    if (vr_check_batch_config(cfg)) return 0;
+    const int64_t cap = cfg->max_indices / cfg->primitive_size;
+    return (cap > 1024 ? cap : 1024) * (int64_t)kGroup * cfg->primitive_size;
+}
+int64_t vr_dynamic_table_words(int64_t n, const vr_batch_config* cfg) {
+    if (vr_check_batch_config(cfg) || n <= 0 || n > 0x7fffffffLL || n % cfg->primitive_size) return 0;
+    return 2 * (int64_t)dyn_layout(n, cfg).cap;
+}
+int vr_dynamic_range_tables(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg, int64_t group_lo, int64_t group_hi,
+                            int32_t* d_table, void* d_ws, size_t ws_bytes, void* stream_) {
+    int st = vr_check_batch_config(cfg);
+    if (st) return st;
+    if (n <= 0 || n % cfg->primitive_size != 0) return VR_ERR_UNALIGNED;
+    if (n > 0x7fffffffLL) return VR_ERR_UNSUPPORTED;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (!d_table) return VR_ERR_BAD_CONFIG;
+    return dyn_launch(1, d_idx, n, cfg, nullptr, 0, (int)group_lo, (int)group_hi, d_table, nullptr, 1, 0, nullptr, nullptr, d_ws, ws_bytes,
+                      (cudaStream_t)stream_);
+}
+int vr_dynamic_range_offsets(const uint32_t* d_idx, int64_t n, const vr_batch_config* cfg, int64_t group_lo, int64_t group_hi,
+                             const int32_t* d_tables, int32_t world, int32_t rank, int32_t* d_offsets, int64_t* d_counts,
+                             void* d_ws, size_t ws_bytes, void* stream_) {
+    int st = vr_check_batch_config(cfg);
+    if (st) return st;
+    if (n <= 0 || n % cfg->primitive_size != 0) return VR_ERR_UNALIGNED;
+    if (n > 0x7fffffffLL) return VR_ERR_UNSUPPORTED;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (!d_tables || !d_offsets || !d_counts || world < 1 || rank < 0 || rank >= world) return VR_ERR_BAD_CONFIG;
+    return dyn_launch(2, d_idx, n, cfg, nullptr, 0, (int)group_lo, (int)group_hi, nullptr, d_tables, world, rank, d_offsets, d_counts, d_ws,
+                      ws_bytes, (cudaStream_t)stream_);
 }
 
 }  // extern "C"

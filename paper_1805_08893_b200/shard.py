@@ -9,10 +9,14 @@ first failing batch in stream order for the error).
 
   static batches   cut points are multiples of batch_size: closed form, no communication
                    (`plan_static`);
-  dynamic batches  a cut must fall on a true greedy boundary, known only after the scan: every rank
-                   runs the index-only boundary scan over the whole stream redundantly (it reads 4 B
-                   per index and writes nothing the other ranks need) and takes its slice of batches
-                   (`plan_from_offsets`; option (i) of SURVEY.md 8e);
+  dynamic batches  a cut must fall on a true greedy boundary, known only after the scan.  Option (ii) of
+                   SURVEY.md 8e (`dynamic_offsets_exchange`, batching="exchange"): every rank scans ITS
+                   range of the stream into a table "entry offset -> (exit offset, batches)", ONE all-gather
+                   of those tables (2.7 KB per rank) composes them, and every rank emits the batches that
+                   start in its range -- the batch formation scales with the ranks, and this all-gather is
+                   the path's one real exchange step.  Option (i) (batching="dynamic"): every rank runs
+                   the index-only boundary scan over the whole stream redundantly and takes its slice of
+                   batches (`plan_from_offsets`); kept for configurations the ranged kernels do not take;
   multi-draw       whole draws per rank, longest-processing-time bin packing (`lpt_assign`), every rank
                    packs and runs its own draws (`run_draws_sharded`).
 
@@ -148,14 +152,78 @@ def plan_from_offsets(offsets, rank: int, world: int) -> ShardPlan:
     return ShardPlan(rank, world, lo, hi, a, b, False)
 
 
+def compose_tables(tables, rank: int):
+    """Host restatement of range_entry_kernel: tables[q] = (exit[cap], count[cap]) of rank q's range; the chain
+    enters range 0 at offset 0.  Returns (entry offset into range `rank`, number of its first batch, total batches)."""
+    t = np.asarray(tables)
+    world, cap = t.shape[0], t.shape[1] // 2
+    e = base = 0
+    entry = (0, 0)
+    for q in range(world):
+        if q == rank:
+            entry = (e, base)
+        base += int(t[q, cap + e])
+        e = int(t[q, e])
+    return entry[0], entry[1], base
+
+
+def dynamic_offsets_exchange(d_indices: torch.Tensor, cfg, rank: int, world: int, group=None, gather=None,
+                             workspace: torch.Tensor | None = None):
+    """batching.py:87-125 over a stream sharded by index range (include/vrgeom.h, vr_dynamic_range_*): this rank's
+    offsets array (the batches that start in its range; positions in the whole buffer), the global number of its
+    first batch and the batch count of the whole stream.  `gather(table) -> [world, words]` replaces the NCCL
+    all-gather (tests run the ranks of a world one after another on one GPU)."""
+    import ctypes as C
+    from . import engine
+
+    lib = N.require_cuda()
+    n = int(d_indices.numel())
+    dev = d_indices.device
+    c = engine._cfg_c(cfg)
+    if n % cfg.primitive_size != 0:
+        from .batching import ConfigError
+        raise ConfigError(f"index count {n} is not primitive-aligned")
+    n_groups = int(lib.vr_dynamic_group_count(n, C.byref(c)))
+    words = int(lib.vr_dynamic_table_words(n, C.byref(c)))
+    glo, ghi = shard_range(n_groups, rank, world)
+    ws_bytes = lib.vr_dynamic_workspace_bytes(n, C.byref(c))
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    table = torch.empty(words, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        engine.raise_status(lib.vr_dynamic_range_tables(engine._ptr(d_indices), n, C.byref(c), glo, ghi, engine._ptr(table),
+                                                        engine._ptr(workspace), ws_bytes, engine._stream_ptr()))
+    if gather is not None:
+        tables = gather(table)
+    elif dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        tables = torch.empty((world, words), dtype=torch.int32, device=dev)
+        dist.all_gather_into_tensor(tables, table, group=group)  # the one exchange step of the path
+    else:
+        tables = table.unsqueeze(0)
+    tables = tables.contiguous()
+    group_prims = int(lib.vr_dynamic_group_indices(C.byref(c))) // cfg.primitive_size
+    cap_out = min(n // cfg.primitive_size, (ghi - glo) * group_prims) + 2
+    offs = torch.empty(cap_out, dtype=torch.int32, device=dev)
+    counts = torch.zeros(4, dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        engine.raise_status(lib.vr_dynamic_range_offsets(engine._ptr(d_indices), n, C.byref(c), glo, ghi, engine._ptr(tables),
+                                                         world, rank, engine._ptr(offs), engine._ptr(counts),
+                                                         engine._ptr(workspace), ws_bytes, engine._stream_ptr()))
+    cnt, status, base, total = (int(v) for v in counts.cpu())
+    if status:
+        engine.raise_status(status)
+    return offs[:cnt + 1], base, total
+
+
 def run_sharded(strategy: str, d_indices: torch.Tensor, cfg, hcfg=None, shader=None, *, batching: str = "static",
                 offsets: torch.Tensor | None = None, rank: int | None = None, world: int | None = None,
                 want_counts: bool = False, buffers=None, group=None, plan_only: bool = False):
     """This rank's share of ONE index stream: (DeviceRun over the rank's batches, ShardPlan).
 
     `d_indices` is the whole stream (replicated, like the vertex buffer: 4 B per index is what a rank needs
-    to find dynamic boundaries on its own).  batching = "static" | "dynamic" | "offsets" (a precomputed
-    device offsets array for the whole stream).  The DeviceRun's outputs are relative to the shard: batch 0
+    to find dynamic boundaries on its own).  batching = "static" | "exchange" (dynamic batches, every rank scans
+    its own range, one all-gather of tables) | "dynamic" (dynamic batches, redundant whole-stream scan) | "offsets"
+    (a precomputed device offsets array for the whole stream).  The DeviceRun's outputs are relative to the shard: batch 0
     is stream batch plan.batch_lo, the assembly map starts at index plan.index_lo."""
     from . import engine
 
@@ -165,6 +233,17 @@ def run_sharded(strategy: str, d_indices: torch.Tensor, cfg, hcfg=None, shader=N
         world = dist.get_world_size(group) if dist.is_initialized() else 1
     n_idx = int(d_indices.numel())
     dev = d_indices.device
+    if batching == "exchange":
+        local, base, _total = dynamic_offsets_exchange(d_indices, cfg, rank, world, group)
+        nb = int(local.numel()) - 1
+        max_span = max(cfg.batch_size, cfg.max_indices - cfg.max_indices % cfg.primitive_size)
+        if nb <= 0:
+            return None, ShardPlan(rank, world, base, base, 0, 0, False)
+        ends = local[[0, nb]].cpu()
+        plan = ShardPlan(rank, world, base, base + nb, int(ends[0]), int(ends[1]), False)
+        run = engine.run_device(strategy, d_indices, local[:-1], local[1:], nb, plan.span, max_span, cfg, hcfg, shader,
+                                want_counts=want_counts, buffers=buffers, contiguous=True, plan_only=plan_only)
+        return run, plan
     if batching == "static":
         plan = plan_static(n_idx, cfg, rank, world)
         offs = engine.static_offsets_device(n_idx, cfg, dev) if offsets is None else offsets

@@ -179,3 +179,63 @@ def test_sharded_multidraw_scene(cuda_lib):
             tot[6] = max(tot[6], st[6])
         assert [got[d] for d in range(len(meshes))] == want
         assert np.array_equal(tot[:7], whole.stats()[:7])
+
+
+@pytest.mark.parametrize("cfgv", [(256, 1023, 3), (64, 255, 3), (256, 1023, 1), (40, 96, 3)])
+def test_ranged_batch_formation_equals_the_whole_stream_scan(cuda_lib, cfgv):
+    """SURVEY.md 8e option (ii): every rank scans its own range of the stream into an entry -> exit table, the tables
+    are gathered (here: the ranks of a world run one after another on this GPU), every rank emits the batches that
+    start in its range.  The concatenation must be vr_dynamic_batches' array, for any world size -- including
+    worlds with more ranks than groups (empty ranges)."""
+    from paper_1805_08893_b200 import shard
+    import torch
+    mu, mi, ps = cfgv
+    cfg = BatchConfig(max_unique=mu, max_indices=mi, primitive_size=ps, batch_size=96 if ps == 3 else 97)
+    mesh = P.shuffle_triangles(P.gen_grid(300, 290), 2) if mu != 64 else P.gen_grid(300, 290)
+    idx = mesh.indices if ps == 3 else mesh.indices[:400_001]
+    d_idx = engine.to_device_indices(idx)
+    whole = engine.dynamic_offsets_device(d_idx, cfg).cpu().numpy()
+    assert np.array_equal(whole, O.dynamic_batches(idx, primitive_size=ps, max_unique=mu, max_indices=mi))
+    for world in (1, 2, 3, 5, 16):
+        ws = [None] * world
+        tables = []
+        import ctypes as C
+        lib = N.require_cuda()
+        c = engine._cfg_c(cfg)
+        n = len(idx)
+        ng, words = lib.vr_dynamic_group_count(n, C.byref(c)), lib.vr_dynamic_table_words(n, C.byref(c))
+        ws_bytes = lib.vr_dynamic_workspace_bytes(n, C.byref(c))
+        for r in range(world):  # step 1 on every rank
+            ws[r] = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+            glo, ghi = shard.shard_range(ng, r, world)
+            t = torch.empty(words, dtype=torch.int32, device="cuda")
+            engine.raise_status(lib.vr_dynamic_range_tables(engine._ptr(d_idx), n, C.byref(c), glo, ghi, engine._ptr(t),
+                                                            engine._ptr(ws[r]), ws_bytes, engine._stream_ptr()))
+            tables.append(t)
+        gathered = torch.stack(tables)  # step 2: the all-gather
+        parts, total_seen, next_base = [], None, 0
+        for r in range(world):  # step 3 on every rank
+            local, base, total = shard.dynamic_offsets_exchange(d_idx, cfg, r, world, gather=lambda t: gathered, workspace=ws[r])
+            e, b, tot = shard.compose_tables(gathered.cpu().numpy(), r)
+            assert (b, tot) == (base, total) == (next_base, len(whole) - 1), (world, r)
+            local = local.cpu().numpy()
+            next_base += len(local) - 1
+            if len(local) > 1:
+                parts.append(local[:-1])
+                closing = local[-1]
+        got = np.concatenate(parts + [[closing]])
+        assert np.array_equal(got, whole), (cfgv, world)
+
+
+def test_sharded_run_with_exchanged_boundaries(cuda_lib):
+    """run_sharded(batching='exchange') at world 1 (no process group) equals the unsharded run."""
+    from paper_1805_08893_b200 import shard
+    mesh = P.shuffle_triangles(P.gen_grid(200, 180), 3)
+    cfg, hc = BatchConfig(), HashConfig()
+    d_idx = engine.to_device_indices(mesh.indices)
+    spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                             matrix=MATRIX, vertex_count=mesh.vertex_count)
+    a, plan_a = shard.run_sharded("hash", d_idx, cfg, hc, spec, batching="exchange", rank=0, world=1)
+    b, plan_b = shard.run_sharded("hash", d_idx, cfg, hc, spec, batching="dynamic", rank=0, world=1)
+    assert (plan_a.batch_lo, plan_a.batch_hi, plan_a.index_lo, plan_a.index_hi) == (plan_b.batch_lo, plan_b.batch_hi, plan_b.index_lo, plan_b.index_hi)
+    assert_flat_equal(a.flat(), b.flat(), "exchange vs whole-stream scan")

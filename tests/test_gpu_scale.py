@@ -210,3 +210,39 @@ def test_sort_long_static_batches_both_kernels(cuda_lib):
         run = engine.run_device("sort", d_idx, offs[:-1], offs[1:], offs.numel() - 1, n_idx, 768, cfg, None,
                                 engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
         assert_flat_equal(run.flat(), oracle_flat(fr), f"static-768 sort, {len(so) - 1} batches")
+
+
+def test_config4_boundary_exchange_world8(cuda_lib, dragon_grid):
+    """configs[3] 'sharded over 2/4/8 GPUs': the shuffled 7.2 M-triangle stream cut into 8 index ranges; every rank's
+    range tables, one gather, every rank's offsets (shard.dynamic_offsets_exchange, the ranks run one after another
+    here).  Their concatenation must be the 84 672 boundaries of the whole-stream scan."""
+    import ctypes as C
+    import torch
+    from paper_1805_08893_b200 import shard
+    mesh = P.shuffle_triangles(dragon_grid, 0)
+    cfg = BatchConfig()
+    d_idx = engine.to_device_indices(mesh.indices)
+    whole = engine.dynamic_offsets_device(d_idx, cfg)
+    lib = N.require_cuda()
+    c = engine._cfg_c(cfg)
+    n = len(mesh.indices)
+    world = 8
+    ng, words = lib.vr_dynamic_group_count(n, C.byref(c)), lib.vr_dynamic_table_words(n, C.byref(c))
+    ws_bytes = lib.vr_dynamic_workspace_bytes(n, C.byref(c))
+    ws, tables = [], []
+    for r in range(world):
+        ws.append(torch.empty(ws_bytes, dtype=torch.uint8, device="cuda"))
+        glo, ghi = shard.shard_range(ng, r, world)
+        t = torch.empty(words, dtype=torch.int32, device="cuda")
+        engine.raise_status(lib.vr_dynamic_range_tables(engine._ptr(d_idx), n, C.byref(c), glo, ghi, engine._ptr(t),
+                                                        engine._ptr(ws[r]), ws_bytes, engine._stream_ptr()))
+        tables.append(t)
+    gathered = torch.stack(tables)
+    parts, seen = [], 0
+    for r in range(world):
+        local, base, total = shard.dynamic_offsets_exchange(d_idx, cfg, r, world, gather=lambda t: gathered, workspace=ws[r])
+        assert base == seen and total == whole.numel() - 1 == 84672
+        seen += local.numel() - 1
+        parts.append(local[:-1])
+        last = local[-1:]
+    assert torch.equal(torch.cat(parts + [last]), whole)

@@ -196,3 +196,67 @@ def test_two_rank_draw_sharding_matches_single_process():
     assert (total[N.VR_STAT_INDICES], total[N.VR_STAT_INVOCATIONS], total[N.VR_STAT_BATCHES]) == (want["i"], want["v"], want["b"])
     assert (total[N.VR_STAT_ROUNDS], total[N.VR_STAT_PROBES_FAST], total[N.VR_STAT_PROBE_MAX_CHAIN]) == (want["r"], want["p"], want["c"])
     assert total[N.VR_STAT_ERROR] == -1
+
+
+def _exchange_worker(rank, world, port, q):
+    """SURVEY.md 8e option (ii) on the host: this rank scans ITS range of the stream into the table "entry offset ->
+    (exit offset, batches)" (the oracle's greedy splitter, restarted at every start primitive of the range, stands in
+    for the device's stage A), ONE all-gather of the tables, shard.compose_tables gives the true entry, the rank
+    emits the batches that start in its range."""
+    import oracle as O
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _, idx = O.gen_grid(31, 29)
+    idx = O.shuffle_triangles(idx, 5) if hasattr(O, "shuffle_triangles") else idx
+    mu, mi, ps = 24, 95, 3
+    cap = mi // ps
+    T = len(idx) // ps
+    s_lo, s_hi = shard.shard_range(T, rank, world)
+
+    def next_of(s):  # end of the greedy batch that starts at primitive s (batching.py:101-123)
+        return s + int(O.dynamic_batches(idx[ps * s:ps * min(T, s + cap + 1)], max_unique=mu, max_indices=mi)[1]) // ps
+
+    nxt = {s: next_of(s) for s in range(s_lo, s_hi)}
+    table = torch.zeros(2 * cap, dtype=torch.int32)
+    for o in range(cap):
+        s, cnt = s_lo + o, 0
+        while s < s_hi:
+            s, cnt = nxt[s], cnt + 1
+        table[o], table[cap + o] = s - s_hi, cnt
+    gathered = [torch.zeros_like(table) for _ in range(world)]
+    dist.all_gather(gathered, table)  # the exchange
+    entry, base, total = shard.compose_tables(torch.stack(gathered).numpy(), rank)
+    mine, s = [], s_lo + entry
+    while s < s_hi:
+        mine.append(ps * s)
+        s = nxt[s]
+    assert len(mine) == int(table[cap + entry])
+    out = [None] * world
+    dist.all_gather_object(out, (base, total, mine))
+    if rank == 0:
+        q.put(out)
+    dist.destroy_process_group()
+
+
+def test_two_and_three_rank_boundary_exchange_matches_the_sequential_scan():
+    import oracle as O
+    _, idx = O.gen_grid(31, 29)
+    idx = O.shuffle_triangles(idx, 5) if hasattr(O, "shuffle_triangles") else idx
+    want = O.dynamic_batches(idx, max_unique=24, max_indices=95)
+    for world in (2, 3):
+        ctx = mp.get_context("spawn")
+        q = ctx.Queue()
+        port = _free_port()
+        procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+        for p in procs:
+            p.start()
+        out = q.get(timeout=180)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+        offs, seen = [], 0
+        for base, total, mine in out:
+            assert base == seen and total == len(want) - 1
+            offs += mine
+            seen += len(mine)
+        assert np.array_equal(np.array(offs + [len(idx)]), want)
