@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
                 const int d = nu + __popc(m & lt);
                 nu += __popc(m);
                 if (nu > g.u_bound) { overflow = true; break; }  // uniform
+                // (every lane's read of kpos above feeds the ballot, so it is complete here; the barrier states it)
+                if (ORDERED) __syncwarp();
                 if (first) {
                     if (ORDERED) kpos[h] = (uint32_t)d; else kidx[h] = (uint16_t)d;
                     dist[d] = id;
