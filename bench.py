@@ -535,9 +535,11 @@ def main():
         inv_cap = int(inv * 1.05) + 1024
         for s in slots:  # the records cross PCIe in the reference's layout (float32[3]), packed on the device
             s["xyz"] = torch.empty((inv_cap, 3), dtype=torch.float32, device=dev)
+            s["map8"] = torch.empty(n_idx + 16, dtype=torch.uint8, device=dev)  # ... and the local indices as bytes
+            s["flag"] = torch.zeros(1, dtype=torch.int32, device=dev)
         host = dict(shaded=torch.empty((inv_cap, 3), dtype=torch.float32).pin_memory(),
                     uid=torch.empty(inv_cap, dtype=torch.int32).pin_memory(),
-                    amap=torch.empty(n_idx, dtype=torch.int16).pin_memory(),
+                    amap=torch.empty(n_idx, dtype=torch.uint8).pin_memory(), flag=torch.zeros(1, dtype=torch.int32).pin_memory(),
                     bro=torch.empty(nb + 1, dtype=torch.int32).pin_memory(),
                     ruo=torch.empty(rounds_cap + 1, dtype=torch.int32).pin_memory(),
                     rp=torch.empty(rounds_cap, dtype=torch.int32).pin_memory())
@@ -572,12 +574,13 @@ def main():
                 s_out.wait_event(s["ev_run"])
                 host["shaded"][:u].copy_(p.shaded_xyz(u, s["xyz"]), non_blocking=True)
                 host["uid"][:u].copy_(p.unique_ids[:u], non_blocking=True)
-                host["amap"][:m].copy_(p.assembly_map[:m], non_blocking=True)
+                host["amap"][:m].copy_(p.assembly_map_u8(m, s["map8"], s["flag"]), non_blocking=True)
+                host["flag"].copy_(s["flag"], non_blocking=True)
                 host["bro"].copy_(p.batch_round_off[:nb + 1], non_blocking=True)
                 host["ruo"][:r + 1].copy_(p.round_uid_off[:r + 1], non_blocking=True)
                 host["rp"][:r].copy_(p.round_prims[:r], non_blocking=True)
                 s["ev_out"].record()
-            d2h[0] += u * 12 + u * 4 + m * 2 + (nb + 1) * 4 + (r + 1) * 4 + r * 4
+            d2h[0] += u * 12 + u * 4 + m * 1 + 4 + (nb + 1) * 4 + (r + 1) * 4 + r * 4
 
         def loop(k_steps, full_result):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -608,6 +611,7 @@ def main():
         p = np.hstack([mesh.positions[uid], np.ones((len(uid), 1))]) @ MATRIX.T
         # (the last loop was stats-only, the host buffers still hold the last full-result step)
         np.testing.assert_allclose(host["shaded"][:inv:997, :3].numpy(), p[:, :3] / p[:, 3:4], rtol=1e-5, atol=1e-5)
+        assert int(host["flag"][0]) == 0, "a local index did not fit a byte"
         return {"value": out["full_result"]["value"], "unit": UNIT,
                 "h2d_bytes_per_step": int(h_idx.numel() * 4 + h_pos.numel() * 4),
                 "d2h_bytes_per_step": out["full_result"]["d2h_bytes_per_step"], "steps": e2e_steps,
@@ -615,7 +619,7 @@ def main():
                 "stats_only": out["stats_only"],
                 "note": "pinned host index buffer (uint32) + vertex buffer (3 x fp32, packed to float4 on the device) copied in "
                         "every step; offsets resident; the whole result copied back to pinned host memory every step (shaded "
-                        "vertices as the reference's float32[3] records, packed on the device; unique ids, uint16 local-index triangles, round tables, statistics); copy-in, "
+                        "vertices as the reference's float32[3] records and local-index triangles as bytes, both packed on the device; unique ids, round tables, statistics); copy-in, "
                         "kernels and copy-out of consecutive steps overlap on three streams (two device slots); "
                         "'stats_only' = same loop with only the 128-byte statistics block read back"}
 

@@ -249,6 +249,10 @@ int vr_expand_stream(const int32_t *d_batch_round_off, const int32_t *d_round_ui
 /* strategies.py:53-67 records are float32[3] (x/w, y/w, z/w); the stage keeps float4 (+ w) for 16-byte stores.
  * Packs d_shaded4[n] to float[3*n] -- what a caller copies to the host when it wants the reference's record. */
 int vr_pack_xyz(const float *d_shaded4, int64_t n, float *d_xyz, void *stream);
+/* Local indices are < warp_width (warp voting) or < max_unique (sort / hash), i.e. bytes for every configuration of
+ * the paper: packs d_assembly_map[n] (uint16) to uint8[n] for the trip to the host.  d_flag (device int32[1], may be
+ * NULL) is set to 1 if a value did not fit. */
+int vr_pack_bytes(const uint16_t *d_assembly_map, int64_t n, uint8_t *d_out, int32_t *d_flag, void *stream);
 
 /* Same walk as vr_expand_stream, but out[slot] = round base + assembly_map[slot]: the position of the
  * slot's record in the unique-id / shaded arrays (int32[n_slots]).  Clients that attach their own

@@ -1681,6 +1681,27 @@ __global__ void __launch_bounds__(256) pack_xyz_kernel(const float4* __restrict_
     }
 }
 
+// uint16 local indices -> bytes, 16 per thread (the map is padded to a multiple of 8 entries by every caller of vr_run)
+__global__ void __launch_bounds__(256) pack_u8_kernel(const uint16_t* __restrict__ in, int64_t n, uint8_t* __restrict__ out, int32_t* flag) {
+    const int64_t i = 16 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (i >= n) return;
+    uint32_t big = 0;
+    if (i + 16 <= n && (((uintptr_t)(in + i)) & 15) == 0 && (((uintptr_t)(out + i)) & 15) == 0) {
+        const uint4 a = *reinterpret_cast<const uint4*>(in + i), b = *reinterpret_cast<const uint4*>(in + i + 8);
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+        uint32_t o[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            big |= (w[2 * k] | w[2 * k + 1]) & 0xFF00FF00u;
+            o[k] = __byte_perm(w[2 * k], w[2 * k + 1], 0x6420);
+        }
+        *reinterpret_cast<uint4*>(out + i) = make_uint4(o[0], o[1], o[2], o[3]);
+    } else {
+        for (int64_t k = i; k < n && k < i + 16; k++) { big |= in[k] & 0xFF00u; out[k] = (uint8_t)in[k]; }
+    }
+    if (big && flag) *flag = 1;
+}
+
 __global__ void static_offsets_kernel(int64_t n, int bs, int64_t nb, int32_t* __restrict__ off) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nb) off[i] = (int32_t)(i * bs);
@@ -2180,6 +2201,16 @@ int vr_pack_xyz(const float* d_shaded4, int64_t n, float* d_xyz, void* stream) {
     if (n == 0) return VR_OK;
     if (!d_shaded4 || !d_xyz || ((uintptr_t)d_xyz & 15) || ((uintptr_t)d_shaded4 & 15)) return VR_ERR_BAD_CONFIG;
     pack_xyz_kernel<<<(int)ceil_div(ceil_div(n, 4), 256), 256, 0, (cudaStream_t)stream>>>((const float4*)d_shaded4, n, d_xyz);
+    VR_CUDA_CHECK(cudaGetLastError());
+    return VR_OK;
+}
+
+int vr_pack_bytes(const uint16_t* d_map, int64_t n, uint8_t* d_out, int32_t* d_flag, void* stream) {
+    if (n < 0) return VR_ERR_BAD_CONFIG;
+    if (vr_device_count() == 0) return VR_ERR_CUDA;
+    if (n == 0) return VR_OK;
+    if (!d_map || !d_out) return VR_ERR_BAD_CONFIG;
+    pack_u8_kernel<<<(int)ceil_div(ceil_div(n, 16), 256), 256, 0, (cudaStream_t)stream>>>(d_map, n, d_out, d_flag);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
 }

@@ -241,6 +241,18 @@ class DeviceRun:
             raise_status(lib.vr_pack_xyz(_ptr(self.shaded4), n, _ptr(out), _stream_ptr()))
         return out[:n]
 
+    def assembly_map_u8(self, count: int | None = None, out: torch.Tensor | None = None, flag: torch.Tensor | None = None):
+        """The local indices as bytes (vr_pack_bytes): they are < warp_width resp. <= max_unique <= 256 in every configuration
+        of the paper, and half as many bytes cross PCIe.  `flag` (int32[1], zeroed by the caller) is set if one did not fit."""
+        lib = N.require_cuda()
+        n = self.indices if count is None else count
+        if out is None:
+            out = torch.empty(n + 16, dtype=torch.uint8, device=self.stats_dev.device)
+        with torch.cuda.device(self.stats_dev.device):
+            raise_status(lib.vr_pack_bytes(_ptr(self.assembly_map), n, _ptr(out), _ptr(flag) if flag is not None else None,
+                                        _stream_ptr()))
+        return out[:n]
+
     def expand_stream(self, positions: bool):
         """Per-corner record stream (strategies.py:456-463) built on the device."""
         self.check()

@@ -137,3 +137,15 @@ def test_pack_xyz(cuda_lib):
     for count in (run.invocations, run.invocations - 1, run.invocations - 2, run.invocations - 3, 1):
         xyz = run.shaded_xyz(count).cpu().numpy()
         assert xyz.shape == (count, 3) and np.array_equal(xyz, run.shaded4[:count, :3].cpu().numpy())
+    # vr_pack_bytes: the local indices as bytes
+    import torch
+    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for count in (run.indices, run.indices - 5, 17, 1):
+        m8 = run.assembly_map_u8(count, flag=flag).cpu().numpy()
+        assert np.array_equal(m8.astype(np.int32), run.flat()["assembly_map"][:count])
+    assert int(flag.item()) == 0
+    big = run.assembly_map.clone()
+    big[3] = 300
+    run.assembly_map = big
+    run.assembly_map_u8(64, flag=flag)
+    assert int(flag.item()) == 1
