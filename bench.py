@@ -488,22 +488,21 @@ def main():
             res["incl_batch_formation"] = {"ms_per_step": t_whole, "value": world * tris / (t_whole * 1e-3),
                                            "algorithmic_bytes": alg_w, "frac": alg_w / (t_whole * 1e-3) / 1e9 / peak}
         if name in ("c3_warp", "c4_sort"):
-            # the paper's stage output is the expanded per-corner queue (strategies.py:456-463): the
-            # stage followed by vr_expand_stream (a post-pass kernel), with the queue's writes in the denominator:
-            # + 2 B local index and 16 B shaded record read, 12 B float32[3] record written per corner
-            saved_stats = run.check().stats().copy()
-
-            def with_queue():
-                r = step()
-                r._stats = saved_stats  # (sizes are known: no host round trip inside the timed region)
-                r.expand_stream(True)
-            with_queue()
+            # the paper's stage output is the expanded per-corner queue (strategies.py:456-463), written
+            # by the stage itself (kernel C of the sort/hash path) or by vr_run's closing kernel (tile kernel path),
+            # with the queue in the denominator: + 12 B float32[3] record written per corner (and, for the closing
+            # kernel, 2 B local index + 16 B record read)
+            qplan = engine.run_device(wl["strategy"], d_idx, offs[:-1], offs[1:], nb, n_idx, max_span, cfg, hcfg, spec,
+                                      buffers=engine.RunBuffers(), static=static, want_queue=True, plan_only=True)
+            with_queue = qplan.relaunch  # the queue is an output of vr_run (vr_outputs.d_stream_xyz)
+            with_queue().check()
             q_steps = max(5, min(steps, 20))
             t_q = timed_steps(with_queue, q_steps)[0] / q_steps
             alg_q = alg + n_idx * 12
             res["expanded_queue"] = {"ms_per_step": t_q, "value": world * tris / (t_q * 1e-3), "algorithmic_bytes": alg_q,
                                      "frac": alg_q / (t_q * 1e-3) / 1e9 / peak,
-                                     "note": "stage + per-corner record queue (float32[3] per corner, post-pass kernel)"}
+                                     "launches_per_step": lib.vr_last_launch_count(),
+                                     "note": "stage incl. the per-corner record queue (float32[3] per corner, vr_outputs.d_stream_xyz)"}
         if not full:
             return res, None
         return res, run_e2e(wl, mesh, cfg, hcfg, offs, nb, max_span, static, inv, steps)

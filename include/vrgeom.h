@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define VRGEOM_ABI_VERSION 3
+#define VRGEOM_ABI_VERSION 4
 
 /* strategies.py:387  STRATEGY_NAMES = ("naive", "warp", "sort", "hash", "phash") */
 enum vr_strategy {
@@ -152,6 +152,12 @@ typedef struct vr_outputs {
     int64_t *d_stats;           /* [VR_STATS_WORDS]                                          */
     int64_t cap_unique;         /* capacity of d_unique_ids / d_shaded4 (elements)           */
     int64_t cap_rounds;         /* capacity of d_round_prims (elements)                      */
+    float *d_stream_xyz;        /* optional, VR_SHADER_POSITION: the stage's output QUEUE (strategies.py:456-463,
+                                   PAPER.md:656), float[3 * sum of batch spans]: the record of every corner,
+                                   out[slot] = shaded[round base + assembly_map[slot]].xyz.  Written inside the
+                                   stage by the three-kernel sort/hash path (from the shaded records in shared
+                                   memory), by a closing kernel of vr_run on the other paths.  Needs the round
+                                   tables and d_assembly_map.  NULL = no queue (vr_expand_stream builds it later) */
 } vr_outputs;
 
 int vr_abi_version(void);

@@ -7,7 +7,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libvrgeom.so")
-ABI_VERSION = 3  # VRGEOM_ABI_VERSION of include/vrgeom.h this binding was written against
+ABI_VERSION = 4  # VRGEOM_ABI_VERSION of include/vrgeom.h this binding was written against
 
 VR_NAIVE, VR_WARP, VR_SORT, VR_HASH, VR_PHASH = range(5)
 STRATEGY_IDS = {"naive": VR_NAIVE, "warp": VR_WARP, "sort": VR_SORT, "hash": VR_HASH, "phash": VR_PHASH}
@@ -60,7 +60,7 @@ class OutputsC(C.Structure):
                 ("d_round_prims", C.c_void_p), ("d_unique_ids", C.c_void_p),
                 ("d_assembly_map", C.c_void_p), ("d_shaded4", C.c_void_p),
                 ("d_shaded_attr", C.c_void_p), ("d_shade_counts", C.c_void_p), ("d_stats", C.c_void_p),
-                ("cap_unique", C.c_int64), ("cap_rounds", C.c_int64)]
+                ("cap_unique", C.c_int64), ("cap_rounds", C.c_int64), ("d_stream_xyz", C.c_void_p)]
 
 
 class CacheConfigC(C.Structure):

@@ -362,13 +362,19 @@ __device__ __forceinline__ void warp_bitonic_blocked(uint32_t (&v)[R], int lane)
     }
 }
 
-template <int STRATEGY>
+// QUEUE: also write the stage's output queue (vr_outputs.d_stream_xyz) -- a separate instantiation, so that the
+// default kernel's register allocation does not pay for it
+template <int STRATEGY, bool QUEUE>
 __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx c, ShaderParams sp, Dyn3Geom g) {
     __shared__ __align__(16) uint32_t s_list[kDyn3Warps][256];  // the round's unique ids, in output order
     __shared__ __align__(16) uint16_t s_of_d[kDyn3Warps][256];  // per distinct id d: distance home -> slot << 8 | position in the list
     __shared__ uint32_t s_bm[kDyn3Warps][16];                   // hash: occupancy words, their exclusive popcount prefix
+    extern __shared__ __align__(16) unsigned char smem_raw[];   // the batch's shaded records [warp][256] when the queue is wanted
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int b = blockIdx.x * kDyn3Warps + wid;
+    float* __restrict__ queue = QUEUE ? c.out.d_stream_xyz : nullptr;
+    float4* kept = QUEUE ? reinterpret_cast<float4*>(smem_raw) + 256 * wid : nullptr;
+    float* qstage = QUEUE ? reinterpret_cast<float*>(smem_raw) + 4 * 256 * kDyn3Warps + 96 * wid : nullptr;  // one row of records
     if (b < c.n_batches && !c.acc[ACC_ABORT]) {
         const int2 cnt = c.counts[b];
         const int2 off = c.seg_off[b];
@@ -491,9 +497,19 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
             // local indices (and the probe statistics of every element, duplicates included)
             unsigned int fast = 0, slow = 0, cmax = 0;
             const int wshift = ilog2((uint32_t)g.w);
+            // with the output queue (strategies.py:456-463) the records are shaded first and kept in shared memory:
+            // a corner's record is then one more shared-memory read next to its local index
+            if (QUEUE) {
+                shade_stream<VR_SORT>(c, sp, list, nu, off.y, lane, 32, mo, vbase, b, kept);
+                __syncwarp();
+            }
             auto element = [&](int i, uint32_t dnum) {
                 const uint32_t e = of_d[dnum & 0xFFu];
                 amap[i] = (uint16_t)(e & 0xFFu);
+                if (QUEUE) {  // the corner's record, on its way out through the warp's staging row (see queue_row)
+                    const float4 rec = kept[e & 0xFFu];
+                    qstage[3 * lane + 0] = rec.x; qstage[3 * lane + 1] = rec.y; qstage[3 * lane + 2] = rec.z;
+                }
                 if (STRATEGY != VR_SORT) {
                     const uint32_t dd = e >> 8;  // chain - 1 (strategies.py:277-297)
                     if (STRATEGY == VR_HASH || dd < (uint32_t)g.mfp) {
@@ -505,10 +521,27 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
                     cmax = max(cmax, dd + 1);
                 }
             };
+            // The 32 records of a step are 96 consecutive floats of the queue: written as three fully coalesced 4-byte
+            // stores per lane (word l, l + 32, l + 64 of the row) after a transposition through shared memory -- a
+            // lane storing its own 12-byte record would touch 12 sectors per instruction instead of 4.
+            auto queue_row = [&](int i0) {
+                __syncwarp();
+                const int words = 3 * min(32, n - i0);
+                float* q = queue + 3 * ((int64_t)mo + i0);
 #pragma unroll
-            for (int k = 0; k < EA; k++)
+                for (int k = 0; k < 3; k++)
+                    if (lane + 32 * k < words) q[lane + 32 * k] = qstage[lane + 32 * k];
+                __syncwarp();
+            };
+#pragma unroll
+            for (int k = 0; k < EA; k++) {
                 if (lane + 32 * k < n) element(lane + 32 * k, early[k]);
-            for (int i = lane + 32 * EA; i < n; i += 32) element(i, amap[i]);
+                if (QUEUE && 32 * k < n) queue_row(32 * k);
+            }
+            for (int i0 = 32 * EA; i0 < n; i0 += 32) {
+                if (i0 + lane < n) element(i0 + lane, amap[i0 + lane]);
+                if (QUEUE) queue_row(i0);
+            }
             if (STRATEGY != VR_SORT) {
                 fast = __reduce_add_sync(0xffffffffu, fast);
                 slow = __reduce_add_sync(0xffffffffu, slow);
@@ -519,7 +552,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
                     atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)cmax);
                 }
             }
-            shade_stream<VR_SORT>(c, sp, list, nu, off.y, lane, 32, mo, vbase, b);
+            if (!QUEUE) shade_stream<VR_SORT>(c, sp, list, nu, off.y, lane, 32, mo, vbase, b);
         }
     }
     // the last CTA to finish writes the statistics block (every CTA's probe counts are in by then)

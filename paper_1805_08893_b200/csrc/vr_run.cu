@@ -1447,7 +1447,8 @@ constexpr int kShadeUnroll = 4;
 // (l = lane within the group): coalesced id load, 16-byte gather, transform, coalesced stores.
 template <int STRATEGY>
 __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams& sp, const uint32_t* __restrict__ src,
-                                             int cnt, int64_t dst0, int l, int width, int naive_mo, int vbase, int batch) {
+                                             int cnt, int64_t dst0, int l, int width, int naive_mo, int vbase, int batch,
+                                             float4* keep = nullptr) {
     const bool want_uid = c.out.d_unique_ids != nullptr;
     const bool want_pos = sp.kind == VR_SHADER_POSITION;
     const bool want_attr = sp.attr_words && c.out.d_shaded_attr;
@@ -1477,7 +1478,11 @@ __device__ __forceinline__ void shade_stream(const RunCtx& c, const ShaderParams
             if (j >= cnt) continue;
             if (want_uid) st_stream_u32(out_uid + j, uid[u], pol.stream);
             if (!live[u]) continue;
-            if (want_pos) st_stream_f4(shaded + j, transform_position<true>(sp, p[u]), pol.stream);
+            if (want_pos) {
+                const float4 rec = transform_position<true>(sp, p[u]);
+                st_stream_f4(shaded + j, rec, pol.stream);
+                if (keep) keep[j] = rec;  // (shared memory: the caller expands the batch's corners from it)
+            }
             if (STRATEGY == VR_NAIVE && c.out.d_assembly_map) c.out.d_assembly_map[naive_mo + j] = (uint16_t)(j % c.ps);
             if (want_attr)
                 for (int k = 0; k < sp.attr_words; k++)
@@ -1602,49 +1607,79 @@ __global__ void __launch_bounds__(256) expand_kernel(const int32_t* __restrict__
                                                       const uint32_t* __restrict__ uids, const float4* __restrict__ shaded,
                                                       int n_batches, const int32_t* __restrict__ map_off, int ps,
                                                       float* __restrict__ out_pos3, uint32_t* __restrict__ out_ids,
-                                                      int32_t* __restrict__ out_src) {
-    const int lane = threadIdx.x & 31;
-    const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+                                                      int32_t* __restrict__ out_src, const int32_t* __restrict__ contiguous_begin = nullptr) {
+    __shared__ float s_row[8][96];  // 32 records of a warp on their way out: see below
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int b = blockIdx.x * (blockDim.x >> 5) + wid;
     if (b >= n_batches) return;
-    int m = map_off[b];
+    // (batches that tile one range of the buffer sit in the map where they sit in the buffer: no span scan)
+    int m = contiguous_begin ? contiguous_begin[b] - contiguous_begin[0] : map_off[b];
+    float* row = s_row[wid];
     for (int r = bro[b]; r < bro[b + 1]; r++) {
         const int base = ruo[r];
         const int slots = rprims[r] * ps;
-        for (int k = lane; k < slots; k += 32) {
-            const int src = base + amap[m + k];
-            if (out_src) out_src[m + k] = src;
-            if (out_ids) out_ids[m + k] = uids[src];
+        for (int k0 = 0; k0 < slots; k0 += 32) {
+            const int k = k0 + lane;
+            if (k < slots) {
+                const int src = base + amap[m + k];
+                if (out_src) out_src[m + k] = src;
+                if (out_ids) out_ids[m + k] = uids[src];
+                if (out_pos3) {
+                    const float4 v = shaded[src];
+                    row[3 * lane] = v.x; row[3 * lane + 1] = v.y; row[3 * lane + 2] = v.z;
+                }
+            }
             if (out_pos3) {
-                float4 v = shaded[src];
-                out_pos3[3 * (int64_t)(m + k) + 0] = v.x;
-                out_pos3[3 * (int64_t)(m + k) + 1] = v.y;
-                out_pos3[3 * (int64_t)(m + k) + 2] = v.z;
+                // the 32 records are 96 consecutive floats: three coalesced 4-byte stores per lane instead of a
+                // 12-byte record per lane (12 sectors per store instruction)
+                __syncwarp();
+                const int words = 3 * min(32, slots - k0);
+                float* q = out_pos3 + 3 * (int64_t)(m + k0);
+#pragma unroll
+                for (int w = 0; w < 3; w++)
+                    if (lane + 32 * w < words) q[lane + 32 * w] = row[lane + 32 * w];
+                __syncwarp();
             }
         }
         m += slots;
     }
 }
 
+// Exclusive scan of the batch spans -> position of every batch in the concatenated assembly map.  One CTA; every
+// thread owns a run of consecutive batches (two passes over its run, one CTA-wide scan of the 1024 partial sums) --
+// not a loop of CTA barriers per 1024 batches (0.4 ms for the 225 000 batches of configs[2]).
 __global__ void __launch_bounds__(1024) span_only_scan_kernel(const int32_t* __restrict__ bbegin, const int32_t* __restrict__ bend,
                                                                int n_batches, int32_t* __restrict__ map_off) {
-    __shared__ int scratch[40];
-    __shared__ int chunk[1024];
-    __shared__ long long carry;
-    const int tid = threadIdx.x;
-    if (tid == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < n_batches; base += 1024) {
-        int b = base + tid;
-        chunk[tid] = b < n_batches ? bend[b] - bbegin[b] : 0;
-        __syncthreads();
-        int total = block_exclusive_scan(chunk, 1024, scratch);
-        long long cb = carry;
-        if (b < n_batches) map_off[b] = (int32_t)(cb + chunk[tid]);
-        __syncthreads();
-        if (tid == 0) carry = cb + total;
-        __syncthreads();
+    __shared__ long long wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (n_batches + 1023) >> 10;
+    const int lo = min(n_batches, tid * per), hi = min(n_batches, lo + per);
+    long long mine = 0;
+    for (int b = lo; b < hi; b++) mine += bend[b] - bbegin[b];
+    long long inc = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
     }
-    if (tid == 0) map_off[n_batches] = (int32_t)carry;
+    if (lane == 31) wsum[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        long long x = wsum[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const long long t = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += t;
+        }
+        wsum[lane] = x;
+    }
+    __syncthreads();
+    long long run = (wid ? wsum[wid - 1] : 0) + inc - mine;
+    for (int b = lo; b < hi; b++) {
+        map_off[b] = (int32_t)run;
+        run += bend[b] - bbegin[b];
+    }
+    if (tid == 1023) map_off[n_batches] = (int32_t)wsum[31];
 }
 
 // multi-draw: first vertex of the draw that holds each batch (include/vrgeom.h vr_batch_vertex_base)
@@ -1980,6 +2015,9 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         sp.load_a = 1.0f; sp.load_b = 0.0f;
         if (sp.kind == VR_SHADER_POSITION && (!sp.pos4 || !out->d_shaded4)) return VR_ERR_BAD_CONFIG;
     }
+    const bool want_queue = out->d_stream_xyz != nullptr && sp.kind == VR_SHADER_POSITION && nb > 0;
+    if (want_queue && (!out->d_assembly_map || !out->d_batch_round_off || !out->d_round_uid_off || !out->d_round_prims))
+        return VR_ERR_BAD_CONFIG;
     const int nbi = (int)nb;
     // limits of the CTA-per-batch kernels
     int pmax = 0, nmax = 0, q = 0;
@@ -2040,15 +2078,19 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             }
             prof_mark(stream);
             prof_mark(stream);
-            switch (strategy) {
-            case VR_SORT: dyn3_finish_kernel<VR_SORT><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
-            case VR_HASH: dyn3_finish_kernel<VR_HASH><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
-            default: dyn3_finish_kernel<VR_PHASH><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            const size_t csmem = want_queue ? (size_t)kDyn3Warps * (256 * sizeof(float4) + 96 * sizeof(float)) : 0;  // the batch's shaded records + a row of the queue
+            switch (strategy * 2 + (want_queue ? 1 : 0)) {
+            case VR_SORT * 2: dyn3_finish_kernel<VR_SORT, false><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            case VR_SORT * 2 + 1: dyn3_finish_kernel<VR_SORT, true><<<ftiles, kDyn3Warps * 32, csmem, stream>>>(c, sp, d3.g); break;
+            case VR_HASH * 2: dyn3_finish_kernel<VR_HASH, false><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            case VR_HASH * 2 + 1: dyn3_finish_kernel<VR_HASH, true><<<ftiles, kDyn3Warps * 32, csmem, stream>>>(c, sp, d3.g); break;
+            case VR_PHASH * 2: dyn3_finish_kernel<VR_PHASH, false><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
+            default: dyn3_finish_kernel<VR_PHASH, true><<<ftiles, kDyn3Warps * 32, csmem, stream>>>(c, sp, d3.g); break;
             }
             prof_mark(stream);
             g_last_launches = strategy == VR_SORT ? 3 : 4;
             VR_CUDA_CHECK(cudaGetLastError());
-            return VR_OK;
+            return VR_OK;  // (kernel C wrote the queue)
         } else if (rows) {
             const int bs = cfg->batch_size;
             switch (cfg->warp_width) {
@@ -2124,10 +2166,19 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         }
     }
     prof_mark(stream);
+    // the output queue on the paths that do not write it inside the stage: a closing kernel (strategies.py:456-463)
+    auto closing_queue = [&]() {
+        if (!want_queue) return 0;
+        if (!contiguous) span_only_scan_kernel<<<1, 1024, 0, stream>>>(d_bbegin, d_bend, nbi, c.map_off);
+        expand_kernel<<<(int)ceil_div(nb, 8), 256, 0, stream>>>(out->d_batch_round_off, out->d_round_uid_off, out->d_round_prims,
+                                                                 out->d_assembly_map, nullptr, (const float4*)out->d_shaded4, nbi, c.map_off, ps,
+                                                                 out->d_stream_xyz, nullptr, nullptr, contiguous ? d_bbegin : nullptr);
+        return contiguous ? 1 : 2;
+    };
     if (fused) {
         prof_mark(stream);
         prof_mark(stream);
-        g_last_launches = 2;  // init + one kernel that dedups, places and shades
+        g_last_launches = 2 + closing_queue();  // init + one kernel that dedups, places and shades
         VR_CUDA_CHECK(cudaGetLastError());
         return VR_OK;
     }
@@ -2148,7 +2199,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
         }
     }
     prof_mark(stream);
-    g_last_launches = (nb > 0 ? 3 : 1) + ((!contiguous && nb > 0) ? 1 : 0) + (L.n_scan_tiles ? 3 : 1);
+    g_last_launches = (nb > 0 ? 3 : 1) + ((!contiguous && nb > 0) ? 1 : 0) + (L.n_scan_tiles ? 3 : 1) + closing_queue();
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
 }

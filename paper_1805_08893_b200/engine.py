@@ -162,6 +162,7 @@ class DeviceRun:
         self.stats_dev = None
         self.launches = 0
         self.kernel_path = 0
+        self.stream_xyz = None  # the output queue, when the run was asked for it (want_queue)
         self._stats = None
 
     def relaunch(self) -> "DeviceRun":
@@ -259,6 +260,8 @@ class DeviceRun:
         lib = N.require_cuda()
         m = self.indices
         dev = self.stats_dev.device
+        if positions and self.stream_xyz is not None:  # written by the stage itself
+            return self.stream_xyz[: 3 * m].view(m, 3)
         if positions:
             out = torch.empty((m, 3), dtype=torch.float32, device=dev)
         else:
@@ -312,7 +315,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                shader: ShaderSpec | None = None, *, want_counts: bool = False,
                buffers: RunBuffers | None = None, enforce_budget: bool = True,
                contiguous: bool | None = None, static: bool = False, fuse: bool = True,
-               plan_only: bool = False) -> DeviceRun:
+               want_queue: bool = False, plan_only: bool = False) -> DeviceRun:
     """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back.
     `plan_only` prepares buffers and arguments without launching: `.relaunch()` then issues the same
     run again (same inputs, outputs overwritten) at the cost of one C call, for callers that repeat a
@@ -364,6 +367,10 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         sh.d_attributes = shader.attributes.data_ptr()
         sh.attr_words = words
         run.shaded_attr = g("sattr", max_inv.value * words, torch.int32, dev).view(-1, words)
+    if want_queue:  # the stage's output queue: one float32[3] record per corner (vr_outputs.d_stream_xyz)
+        if shader.kind != N.VR_SHADER_POSITION:
+            raise ConfigError("the output queue holds shaded positions: position shader only")
+        run.stream_xyz = g("queue", span_total * 3 + 16, torch.float32, dev)
     if want_counts:
         if shader.vertex_count <= 0:
             raise ConfigError("per-vertex tallies need vertex_count")
@@ -374,7 +381,8 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         run.shaded4.data_ptr() if run.shaded4 is not None else None,
         run.shaded_attr.data_ptr() if run.shaded_attr is not None else None,
         run.shade_counts.data_ptr() if run.shade_counts is not None else None,
-        run.stats_dev.data_ptr(), max_inv.value, max_rounds.value)
+        run.stats_dev.data_ptr(), max_inv.value, max_rounds.value,
+        run.stream_xyz.data_ptr() if run.stream_xyz is not None else None)
     args = (sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
             span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws), ws.numel())
     run._keep = (ws, shader, c, h, sh, out, d_indices, d_begin, d_end)

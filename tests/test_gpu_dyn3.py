@@ -133,3 +133,34 @@ def test_dyn3_errors(cuda_lib, strategy):
     run = _run(strategy, mesh, bad2, cfg, hc, want_counts=False)
     with pytest.raises(P.ConfigError, match="batch 8\\)"):
         run.check()
+
+
+@pytest.mark.parametrize("strategy", ["naive", "warp", "sort", "hash", "phash"])
+def test_output_queue_written_by_the_stage(cuda_lib, strategy):
+    """vr_outputs.d_stream_xyz (strategies.py:456-463): the per-corner record queue written inside the stage
+    (three-kernel sort/hash path: from the shaded records in shared memory) or by vr_run's closing kernel (other
+    paths) equals the post-pass expansion (vr_expand_stream) and the float64 reference records."""
+    import torch
+    cfg, hc = BatchConfig(), HashConfig()
+    for name, mesh in _meshes().items():
+        dyn = strategy in ("sort", "hash", "phash")
+        offs = O.dynamic_batches(mesh.indices) if dyn else O.static_batches(len(mesh.indices))
+        spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                                 matrix=MATRIX, vertex_count=mesh.vertex_count)
+        o = torch.from_numpy(np.asarray(offs, dtype=np.int32)).cuda()
+        variants = [dict()] if dyn else [dict(), dict(static=True)]
+        if dyn:
+            variants.append(dict(fuse=False))
+        for kw in variants:
+            args = (strategy, engine.to_device_indices(mesh.indices), o[:-1], o[1:], len(offs) - 1, len(mesh.indices),
+                    int(np.diff(offs).max()), cfg, hc, spec)
+            plain = engine.run_device(*args, **kw)
+            want = plain.expand_stream(True).cpu().numpy()
+            run = engine.run_device(*args, want_queue=True, **kw)
+            if dyn and not kw:
+                assert run.kernel_path == DYN3_PATH
+            got = run.expand_stream(True).cpu().numpy()
+            assert got.shape == (len(mesh.indices), 3) and np.array_equal(got, want), (strategy, name, kw)
+            assert_flat_equal(run.flat(), plain.flat(), f"{strategy} {name} {kw}")
+            pos = np.hstack([mesh.positions, np.ones((mesh.vertex_count, 1))]) @ MATRIX.T
+            np.testing.assert_allclose(got, (pos[:, :3] / pos[:, 3:4])[mesh.indices], rtol=1e-5, atol=1e-5)

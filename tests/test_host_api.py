@@ -141,7 +141,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     handle = ctypes.CDLL(build.LIB)
     for name in declared:
         assert hasattr(handle, name), f"{name} not exported"
-    assert _native.lib().vr_abi_version() == _native.ABI_VERSION == 3
+    assert _native.lib().vr_abi_version() == _native.ABI_VERSION == 4
     assert _native.status_string(5).startswith("hash table full")
 
 
