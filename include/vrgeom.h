@@ -332,6 +332,10 @@ int vr_profile_read(float *ms, int cap);
  * kernel with fused look-back + shading, 3 = persistent tile kernel (csrc/vr_warp_rows.cuh), 4 = three-kernel
  * sort / hash / phash path for budgeted batches (csrc/vr_dyn3.cuh). */
 int vr_last_kernel_path(void);
+/* Debugging / ablation knobs (VR_LAG, VR_PREFETCH, VR_LINK_TILE, ...: `DebugKnobs` in csrc/vr_common.cuh) are read
+ * from the environment once per process; this re-reads them.  For tests and sweeps that change a knob between
+ * runs; not for use while another thread is inside the library. */
+int vr_debug_reload_knobs(void);
 
 #ifdef __cplusplus
 }

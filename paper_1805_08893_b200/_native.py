@@ -111,6 +111,7 @@ _SIGNATURES = {
     "vr_profile_enable": (C.c_int, [C.c_int]),
     "vr_last_launch_count": (C.c_int, []),
     "vr_last_kernel_path": (C.c_int, []),
+    "vr_debug_reload_knobs": (C.c_int, []),
     "vr_profile_read": (C.c_int, [C.POINTER(C.c_float), C.c_int]),
     "vr_expand_stream": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,

@@ -51,19 +51,21 @@ struct DebugKnobs {
     int no_pdl = 0;           // VR_NO_PDL        no programmatic dependent launch
     int dyn3_prefetch = 0;    // VR_DYN3_PREFETCH three-kernel path: L2 prefetch of the distinct vertices before the sort
 };
-inline const DebugKnobs& debug_knobs() {
-    static const DebugKnobs k = [] {
-        DebugKnobs d;
-        auto geti = [](const char* name, int& v) { if (const char* e = getenv(name)) v = atoi(e); };
-        auto flag = [](const char* name, int& v) { if (getenv(name)) v = 1; };
-        geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run);
-        flag("VR_GREEDY_GLOBAL", d.greedy_global); flag("VR_WALK_GLOBAL", d.walk_global); flag("VR_SORT_CTA", d.sort_cta);
-        geti("VR_PREFETCH", d.rows_prefetch); geti("VR_LAG", d.rows_lag); flag("VR_NO_PDL", d.no_pdl);
-        geti("VR_DYN3_PREFETCH", d.dyn3_prefetch);
-        return d;
-    }();
+inline DebugKnobs parse_debug_knobs() {
+    DebugKnobs d;
+    auto geti = [](const char* name, int& v) { if (const char* e = getenv(name)) v = atoi(e); };
+    auto flag = [](const char* name, int& v) { if (getenv(name)) v = 1; };
+    geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run);
+    flag("VR_GREEDY_GLOBAL", d.greedy_global); flag("VR_WALK_GLOBAL", d.walk_global); flag("VR_SORT_CTA", d.sort_cta);
+    geti("VR_PREFETCH", d.rows_prefetch); geti("VR_LAG", d.rows_lag); flag("VR_NO_PDL", d.no_pdl);
+    geti("VR_DYN3_PREFETCH", d.dyn3_prefetch);
+    return d;
+}
+inline DebugKnobs& debug_knobs_storage() {
+    static DebugKnobs k = parse_debug_knobs();
     return k;
 }
+inline const DebugKnobs& debug_knobs() { return debug_knobs_storage(); }
 
 // strategies.py:88-91 HashConfig.slot; bits == 0 (table_size 1) -> slot 0.
 __device__ __forceinline__ uint32_t hash_slot(uint32_t vid, uint32_t mult, int bits) {

@@ -2205,6 +2205,10 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
 }
 
 int vr_last_launch_count(void) { return g_last_launches; }
+int vr_debug_reload_knobs(void) {
+    debug_knobs_storage() = parse_debug_knobs();
+    return VR_OK;
+}
 int vr_last_kernel_path(void) { return g_last_path; }
 
 int vr_batch_vertex_base(const int32_t* d_batch_begin, int64_t n_batches, const int32_t* d_draw_index_start,

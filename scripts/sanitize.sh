@@ -60,7 +60,10 @@ so = engine.static_offsets_device(len(grid.indices), cfg)
 spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(grid.positions), matrix=M, vertex_count=grid.vertex_count)
 d_idx = engine.to_device_indices(grid.indices)
 import os
-for _ in range(2):
+for lag in ("3", "40", None):
+    if lag: os.environ["VR_LAG"] = lag
+    else: os.environ.pop("VR_LAG", None)
+    N.lib().vr_debug_reload_knobs()
     r = engine.run_device("warp", d_idx, so[:-1], so[1:], so.numel() - 1, len(grid.indices), 96, cfg, None, spec, static=True).check()
     assert r.kernel_path == 3
 torch.cuda.synchronize()

@@ -27,6 +27,7 @@ for k in range(cases):
     os.environ.pop("VR_LAG", None)
     if lag is not None:
         os.environ["VR_LAG"] = str(lag)
+    N.lib().vr_debug_reload_knobs()  # the knobs are read once per process
     so = O.static_batches(len(mesh.indices), batch_size=bs)
     fr = O.run("warp", mesh.indices, so[:-1], so[1:], warp_width=w)
     offs = engine.static_offsets_device(len(mesh.indices), cfg)

@@ -352,9 +352,26 @@ def test_fallback_kernels_agree(cuda_lib, monkeypatch):
                                 len(mesh.indices), 1023, cfg, None, engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY))
         return offs.cpu().numpy(), run.flat()
 
+    def once_general():  # VR_SORT_CTA acts on the general sort path (the three-kernel path does not take it)
+        offs = engine.dynamic_offsets_device(mesh.indices, cfg)
+        run = engine.run_device("sort", engine.to_device_indices(mesh.indices), offs[:-1], offs[1:], offs.numel() - 1,
+                                len(mesh.indices), 1023, cfg, None, engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY), fuse=False)
+        assert run.kernel_path == 0
+        return run.flat()
+
     offs_a, flat_a = once()
+    gen_a = once_general()
     for k in ("VR_LINKS_WARP", "VR_GREEDY_GLOBAL", "VR_WALK_GLOBAL", "VR_SORT_CTA"):
         monkeypatch.setenv(k, "1")
-    offs_b, flat_b = once()
+    N.lib().vr_debug_reload_knobs()  # the knobs are read once per process
+    try:
+        offs_b, flat_b = once()
+        gen_b = once_general()
+    finally:
+        for k in ("VR_LINKS_WARP", "VR_GREEDY_GLOBAL", "VR_WALK_GLOBAL", "VR_SORT_CTA"):
+            monkeypatch.delenv(k)
+        N.lib().vr_debug_reload_knobs()
     assert np.array_equal(offs_a, offs_b) and np.array_equal(offs_a.astype(np.int64), O.dynamic_batches(mesh.indices))
     assert_flat_equal(flat_a, flat_b, "fallback kernels")
+    assert_flat_equal(gen_a, gen_b, "CTA sort")
+    assert_flat_equal(gen_a, flat_a, "general vs three-kernel sort")

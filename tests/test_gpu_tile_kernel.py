@@ -27,6 +27,7 @@ def tile_run(idx, cfg, spec, counts=False, lag=None):
     old = os.environ.pop("VR_LAG", None)
     if lag is not None:
         os.environ["VR_LAG"] = str(lag)
+    N.lib().vr_debug_reload_knobs()  # the knobs are read once per process
     try:
         run = engine.run_device("warp", d_idx, o[:-1], o[1:], len(so) - 1, len(idx), cfg.batch_size, cfg, None,
                                 spec, want_counts=counts, static=True)
@@ -35,6 +36,7 @@ def tile_run(idx, cfg, spec, counts=False, lag=None):
         os.environ.pop("VR_LAG", None)
         if old is not None:
             os.environ["VR_LAG"] = old
+        N.lib().vr_debug_reload_knobs()
     assert run.kernel_path == 3 and run.launches == 2, "expected init + the persistent tile kernel"
     return run, so
 
