@@ -171,11 +171,23 @@ __global__ void __launch_bounds__(kCacheThreads) cache_sim_kernel(const uint32_t
 constexpr int kWalkMaxCandidates = 1024;  // moves within max_move_distance (797 at the default 16)
 constexpr int kWalkWarps = 4;
 
+constexpr int kWalkMaxDistance = 18;  // 1009 candidate moves; 19 would be 1129
 struct WalkParams {
     int grid_w, grid_h, d, kept, n_g, n_cand;
     double cx[VR_WALK_MAX_GAUSSIANS], cy[VR_WALK_MAX_GAUSSIANS], inv2s2[VR_WALK_MAX_GAUSSIANS], amp[VR_WALK_MAX_GAUSSIANS];
+    // walk.py:85-99: the candidate moves in row-major scan order are the rows dy = -d .. d of a disk; row r holds
+    // dx = -half[r] .. half[r] and starts at candidate number row_start[r].  (Kernel parameters, not a __constant__
+    // table: concurrent calls with different radii must not share state.)
+    short row_start[2 * kWalkMaxDistance + 2];
+    signed char half[2 * kWalkMaxDistance + 1];
 };
-__constant__ signed char c_walk_dx[kWalkMaxCandidates], c_walk_dy[kWalkMaxCandidates];
+// candidate number -> (dx, dy)
+__device__ __forceinline__ void walk_candidate(const WalkParams& p, int k, int& dx, int& dy) {
+    int r = 0;
+    while (p.row_start[r + 1] <= k) r++;
+    dy = r - p.d;
+    dx = k - p.row_start[r] - p.half[r];
+}
 
 // walk.py:110-137 for one cell per warp.  Candidates in row-major scan order (walk.py:85-99); activity =
 // 1e-12 + sum of the Gaussians at the destination, in the order of cfg.gaussians (walk.py:102-109);
@@ -191,8 +203,10 @@ __global__ void __launch_bounds__(kWalkWarps * 32) walk_likelihood_kernel(const 
     double* act = s_act[wid];
     double sum = 0.0;
     int legal = 0;
+    int row = 0;  // row of the lane's current candidate (candidates ascend, so the row only moves forward)
     for (int k = lane; k < p.n_cand; k += 32) {
-        const int dx = c_walk_dx[k], dy = c_walk_dy[k];
+        while (p.row_start[row + 1] <= k) row++;
+        const int dx = k - p.row_start[row] - p.half[row], dy = row - p.d;
         const int tx = x + dx, ty = y + dy;
         double a = -1.0;  // not on the grid
         if (tx >= 0 && tx < p.grid_w && ty >= 0 && ty < p.grid_h) {
@@ -238,8 +252,10 @@ __global__ void __launch_bounds__(kWalkWarps * 32) walk_likelihood_kernel(const 
             if (ob > best || (ob == best && ok < best_k)) { best = ob; best_k = ok; }
         }
         if (lane == 0) {
-            out[3 * j + 0] = (double)c_walk_dx[best_k];
-            out[3 * j + 1] = (double)c_walk_dy[best_k];
+            int bdx, bdy;
+            walk_candidate(p, best_k, bdx, bdy);
+            out[3 * j + 0] = (double)bdx;
+            out[3 * j + 1] = (double)bdy;
             out[3 * j + 2] = best;
             act[best_k] = -1.0;
         }
@@ -348,32 +364,31 @@ int vr_walk_likelihoods(const uint32_t* d_cells, int64_t n, const vr_walk_config
     if (!cfg || !d_status) return VR_ERR_BAD_CONFIG;
     if (cfg->grid_w < 2 || cfg->grid_h < 2 || cfg->grid_w > 65536 || cfg->grid_h > 65536) return VR_ERR_BAD_CONFIG;  // walk.py:62-64
     if (cfg->max_move_distance < 1 || cfg->kept_moves < 1 || cfg->n_gaussians < 0 || cfg->n_gaussians > VR_WALK_MAX_GAUSSIANS) return VR_ERR_BAD_CONFIG;
-    if (cfg->max_move_distance > 127) return VR_ERR_UNSUPPORTED;
-    // walk.py:85-99 candidate moves, row-major scan order
-    static signed char hx[kWalkMaxCandidates], hy[kWalkMaxCandidates];
+    if (cfg->max_move_distance > kWalkMaxDistance) return VR_ERR_UNSUPPORTED;  // more than 1024 candidate moves
+    WalkParams p{};
     const int d = cfg->max_move_distance;
     int nc = 0;
-    for (int dy = -d; dy <= d; dy++)
-        for (int dx = -d; dx <= d; dx++)
-            if (dx * dx + dy * dy <= d * d) {
-                if (nc >= kWalkMaxCandidates) return VR_ERR_UNSUPPORTED;
-                hx[nc] = (signed char)dx; hy[nc] = (signed char)dy; nc++;
-            }
+    for (int dy = -d; dy <= d; dy++) {  // walk.py:85-99 candidate moves, row-major scan order
+        int h = 0;
+        while ((h + 1) * (h + 1) + dy * dy <= d * d) h++;
+        p.row_start[dy + d] = (short)nc;
+        p.half[dy + d] = (signed char)h;
+        nc += 2 * h + 1;
+    }
+    p.row_start[2 * d + 1] = (short)nc;
+    if (nc > kWalkMaxCandidates) return VR_ERR_UNSUPPORTED;
     if (cfg->kept_moves > nc) return VR_ERR_BAD_CONFIG;  // walk.py:69-70
     if (vr_device_count() == 0) return VR_ERR_CUDA;
     cudaStream_t stream = (cudaStream_t)stream_;
     VR_CUDA_CHECK(cudaMemsetAsync(d_status, 0, sizeof(int64_t), stream));
     if (n <= 0) return VR_OK;
     if (!d_cells || !d_moves) return VR_ERR_BAD_CONFIG;
-    WalkParams p{};
     p.grid_w = cfg->grid_w; p.grid_h = cfg->grid_h; p.d = d; p.kept = cfg->kept_moves; p.n_g = cfg->n_gaussians; p.n_cand = nc;
     for (int g = 0; g < cfg->n_gaussians; g++) {
         p.cx[g] = cfg->gaussians[g][0]; p.cy[g] = cfg->gaussians[g][1];
         p.inv2s2[g] = 2.0 * cfg->gaussians[g][2] * cfg->gaussians[g][2];  // walk.py:108
         p.amp[g] = cfg->gaussians[g][3];
     }
-    VR_CUDA_CHECK(cudaMemcpyToSymbolAsync(c_walk_dx, hx, nc, 0, cudaMemcpyHostToDevice, stream));
-    VR_CUDA_CHECK(cudaMemcpyToSymbolAsync(c_walk_dy, hy, nc, 0, cudaMemcpyHostToDevice, stream));
     walk_likelihood_kernel<<<(int)ceil_div(n, kWalkWarps), kWalkWarps * 32, 0, stream>>>(d_cells, n, p, d_moves, (long long*)d_status);
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
