@@ -47,7 +47,11 @@ __device__ __forceinline__ int dyn3_aux_stride(int span) { return (span + 15) & 
 constexpr int kDyn3AuxHome = 32;  // byte offset of home[] behind the bitmap
 
 // ---- A ------------------------------------------------------------------------------------------
-template <bool ORDERED, bool PHASH>
+// WIDE: 64 elements per step, two per lane, their two probe chains interleaved -- for LONG batches (a strip-ordered mesh:
+// ~760 indices per batch): the second chain hides the first one's shared-memory atomic latency.  On the short batches of
+// a shuffled mesh (~255 indices) the 40+ registers cost more resident warps than that saves (measured), so vr_run picks
+// the variant by the average batch length.
+template <bool ORDERED, bool PHASH, bool WIDE>
 __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, Dyn3Geom g) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_tile;
@@ -92,44 +96,95 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
             }
             __syncwarp();
             bool overflow = false;
-            // (two elements per lane and step with interleaved probe chains: measured slower on the short batches of
-            // a shuffled mesh -- 40+ registers instead of 32 cost more warps than the shared ballots saved)
-            for (int i0 = 0; i0 < n; i0 += 32) {
-                const int i = i0 + lane;
-                const bool valid = i < n;
-                const uint32_t id = id_next;
-                if (i + 32 < n) id_next = __ldg(ids + i + 32);
-                uint32_t h = (id * 0x9E3779B1u) >> qshift;
-                bool first = false;
-                if (valid) {
-                    for (;;) {
-                        const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
-                        if (prev == kEmpty) first = true;
-                        if (prev == kEmpty || prev == id) break;
-                        h = (h + 1) & qmask;
+            if (WIDE) {
+                uint32_t next_b = lane + 32 < n ? __ldg(ids + lane + 32) : 0u;
+                for (int i0 = 0; i0 < n; i0 += 64) {
+                    const int ia = i0 + lane, ib = ia + 32;
+                    const bool va = ia < n, vb = ib < n;
+                    const uint32_t id_a = id_next, id_b = next_b;
+                    if (ia + 64 < n) id_next = __ldg(ids + ia + 64);
+                    if (ib + 64 < n) next_b = __ldg(ids + ib + 64);
+                    uint32_t ha = (id_a * 0x9E3779B1u) >> qshift, hb = (id_b * 0x9E3779B1u) >> qshift;
+                    bool first_a = false, first_b = false;
+                    bool pa = va, pb = vb;
+                    while (pa || pb) {
+                        if (pa) {
+                            const uint32_t prev = atomicCAS(&kkey[ha], kEmpty, id_a);
+                            if (prev == kEmpty) first_a = true;
+                            if (prev == kEmpty || prev == id_a) pa = false; else ha = (ha + 1) & qmask;
+                        }
+                        if (pb) {
+                            const uint32_t prev = atomicCAS(&kkey[hb], kEmpty, id_b);
+                            if (prev == kEmpty) first_b = true;
+                            if (prev == kEmpty || prev == id_b) pb = false; else hb = (hb + 1) & qmask;
+                        }
                     }
-                    if (ORDERED) atomicMin(&kpos[h], (uint32_t)i);
-                }
-                if (ORDERED) {
-                    // the reference inserts in batch order: among equal ids of this step the lowest position is the
-                    // first occurrence (ids of earlier steps hold their d, which is below every later position)
+                    if (ORDERED) {
+                        if (va) atomicMin(&kpos[ha], (uint32_t)ia);
+                        if (vb) atomicMin(&kpos[hb], (uint32_t)ib);
+                        __syncwarp();
+                        first_a = va && kpos[ha] == (uint32_t)ia;
+                        first_b = vb && kpos[hb] == (uint32_t)ib;
+                    }
+                    const uint32_t ma = __ballot_sync(0xffffffffu, first_a), mb = __ballot_sync(0xffffffffu, first_b);
+                    const int da = nu + __popc(ma & lt), db = nu + __popc(ma) + __popc(mb & lt);
+                    nu += __popc(ma) + __popc(mb);
+                    if (nu > g.u_bound) { overflow = true; break; }  // uniform
+                    if (ORDERED) __syncwarp();
+                    if (first_a) {
+                        if (ORDERED) kpos[ha] = (uint32_t)da; else kidx[ha] = (uint16_t)da;
+                        dist[da] = id_a;
+                        if (ORDERED) home[da] = (unsigned char)hash_slot(id_a, c.multiplier, c.table_bits);
+                        if (PHASH) grp[da] = (uint16_t)(ia >> wshift);
+                    }
+                    if (first_b) {
+                        if (ORDERED) kpos[hb] = (uint32_t)db; else kidx[hb] = (uint16_t)db;
+                        dist[db] = id_b;
+                        if (ORDERED) home[db] = (unsigned char)hash_slot(id_b, c.multiplier, c.table_bits);
+                        if (PHASH) grp[db] = (uint16_t)(ib >> wshift);
+                    }
                     __syncwarp();
-                    first = valid && kpos[h] == (uint32_t)i;
+                    if (va) dmap[ia] = ORDERED ? (uint16_t)kpos[ha] : kidx[ha];
+                    if (vb) dmap[ib] = ORDERED ? (uint16_t)kpos[hb] : kidx[hb];
                 }
-                const uint32_t m = __ballot_sync(0xffffffffu, first);
-                const int d = nu + __popc(m & lt);
-                nu += __popc(m);
-                if (nu > g.u_bound) { overflow = true; break; }  // uniform
-                // (every lane's read of kpos above feeds the ballot, so it is complete here; the barrier states it)
-                if (ORDERED) __syncwarp();
-                if (first) {
-                    if (ORDERED) kpos[h] = (uint32_t)d; else kidx[h] = (uint16_t)d;
-                    dist[d] = id;
-                    if (ORDERED) home[d] = (unsigned char)hash_slot(id, c.multiplier, c.table_bits);
-                    if (PHASH) grp[d] = (uint16_t)(i >> wshift);
+            } else {
+                for (int i0 = 0; i0 < n; i0 += 32) {
+                    const int i = i0 + lane;
+                    const bool valid = i < n;
+                    const uint32_t id = id_next;
+                    if (i + 32 < n) id_next = __ldg(ids + i + 32);
+                    uint32_t h = (id * 0x9E3779B1u) >> qshift;
+                    bool first = false;
+                    if (valid) {
+                        for (;;) {
+                            const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
+                            if (prev == kEmpty) first = true;
+                            if (prev == kEmpty || prev == id) break;
+                            h = (h + 1) & qmask;
+                        }
+                        if (ORDERED) atomicMin(&kpos[h], (uint32_t)i);
+                    }
+                    if (ORDERED) {
+                        // the reference inserts in batch order: among equal ids of this step the lowest position is the
+                        // first occurrence (ids of earlier steps hold their d, which is below every later position)
+                        __syncwarp();
+                        first = valid && kpos[h] == (uint32_t)i;
+                    }
+                    const uint32_t m = __ballot_sync(0xffffffffu, first);
+                    const int d = nu + __popc(m & lt);
+                    nu += __popc(m);
+                    if (nu > g.u_bound) { overflow = true; break; }  // uniform
+                    // (every lane's read of kpos above feeds the ballot, so it is complete here; the barrier states it)
+                    if (ORDERED) __syncwarp();
+                    if (first) {
+                        if (ORDERED) kpos[h] = (uint32_t)d; else kidx[h] = (uint16_t)d;
+                        dist[d] = id;
+                        if (ORDERED) home[d] = (unsigned char)hash_slot(id, c.multiplier, c.table_bits);
+                        if (PHASH) grp[d] = (uint16_t)(i >> wshift);
+                    }
+                    __syncwarp();
+                    if (valid) dmap[i] = ORDERED ? (uint16_t)kpos[h] : kidx[h];
                 }
-                __syncwarp();
-                if (valid) dmap[i] = ORDERED ? (uint16_t)kpos[h] : kidx[h];
             }
             rounds = 1;
             if (overflow) {  // strategies.py:451-455 / :283-284
@@ -591,7 +646,7 @@ static Dyn3Plan dyn3_plan(int strategy, const vr_batch_config* cfg, const vr_has
         if (strategy == VR_PHASH && (max_span >> ilog2((uint32_t)cfg->warp_width)) > 65535) return p;
     }
     if (g.u_bound > 256) return p;
-    g.q = (int)next_pow2((uint32_t)((g.u_bound + 32) * 3 / 2 + 2));  // the set holds <= u_bound + 32 ids: load <= 2/3
+    g.q = (int)next_pow2((uint32_t)((g.u_bound + 64) * 3 / 2 + 2));  // the set holds <= u_bound + 64 ids: load <= 2/3
     if (g.q < 128) g.q = 128;
     g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4);
     p.smem_a = (size_t)kDyn3Warps * g.per_warp_bytes;

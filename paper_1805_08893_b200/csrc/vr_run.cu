@@ -2064,18 +2064,20 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
             naive_counts_kernel<<<(nbi + 255) / 256, 256, 0, stream>>>(c);
         } else if (d3.ok) {
             const int tiles = c.n_fused_tiles, ftiles = (int)ceil_div(nb, kDyn3Warps);
-            if (strategy == VR_SORT) {
-                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
-                dyn3_dedup_kernel<false, false><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
-            } else if (strategy == VR_HASH) {
-                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
-                dyn3_dedup_kernel<true, false><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
-                dyn3_insert_kernel<false><<<(int)ceil_div(nb, kDyn3InsertThreads), kDyn3InsertThreads, 0, stream>>>(c, d3.g);
-            } else {
-                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_dedup_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a));
-                dyn3_dedup_kernel<true, true><<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
-                dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads / 2), kDyn3InsertThreads / 2, 0, stream>>>(c, d3.g);
-            }
+            // long batches (strip-ordered meshes), sort: two elements per lane and step; see dyn3_dedup_kernel.  (With the
+            // ordered numbering of hash / phash the wide variant measured slower on both kinds of mesh: 58 registers.)
+            const bool wide = strategy == VR_SORT && span_total / nb >= 384;
+            auto launch_a = [&](auto kernel) -> int {
+                if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3.smem_a) != cudaSuccess) return VR_ERR_CUDA;
+                kernel<<<tiles, kDyn3Warps * 32, d3.smem_a, stream>>>(c, d3.g);
+                return VR_OK;
+            };
+            if (strategy == VR_SORT) st = wide ? launch_a(dyn3_dedup_kernel<false, false, true>) : launch_a(dyn3_dedup_kernel<false, false, false>);
+            else if (strategy == VR_HASH) st = launch_a(dyn3_dedup_kernel<true, false, false>);
+            else st = launch_a(dyn3_dedup_kernel<true, true, false>);
+            if (st) return st;
+            if (strategy == VR_HASH) dyn3_insert_kernel<false><<<(int)ceil_div(nb, kDyn3InsertThreads), kDyn3InsertThreads, 0, stream>>>(c, d3.g);
+            if (strategy == VR_PHASH) dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads / 2), kDyn3InsertThreads / 2, 0, stream>>>(c, d3.g);
             prof_mark(stream);
             prof_mark(stream);
             const size_t csmem = want_queue ? (size_t)kDyn3Warps * (256 * sizeof(float4) + 96 * sizeof(float)) : 0;  // the batch's shaded records + a row of the queue
