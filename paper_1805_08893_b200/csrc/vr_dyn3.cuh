@@ -40,6 +40,7 @@ struct Dyn3Geom {
     int strategy;
     int prefetch;        // kernel C: L2 prefetch of the distinct vertices before they are put in order
     unsigned char* aux;  // hash/phash: per batch occupancy bitmap[32 B] | home[span'] | slot[span'] | grp u16[span']
+    float* queue;        // vr_outputs.d_stream_xyz (kernel C with QUEUE)
 };
 
 __device__ __forceinline__ int64_t dyn3_aux_base(const RunCtx& c, int b, int mo) { return ((int64_t)mo * 4 + (int64_t)b * 128) & ~15LL; }
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
     extern __shared__ __align__(16) unsigned char smem_raw[];   // the batch's shaded records [warp][256] when the queue is wanted
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int b = blockIdx.x * kDyn3Warps + wid;
-    float* __restrict__ queue = QUEUE ? c.out.d_stream_xyz : nullptr;
+    float* __restrict__ queue = QUEUE ? g.queue : nullptr;
     float4* kept = QUEUE ? reinterpret_cast<float4*>(smem_raw) + 256 * wid : nullptr;
     float* qstage = QUEUE ? reinterpret_cast<float*>(smem_raw) + 4 * 256 * kDyn3Warps + 96 * wid : nullptr;  // one row of records
     if (b < c.n_batches && !c.acc[ACC_ABORT]) {

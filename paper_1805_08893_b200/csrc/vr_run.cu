@@ -21,6 +21,23 @@ namespace vr {
 
 enum { ACC_PROBES_FAST = 0, ACC_PROBES_SLOW, ACC_MAX_CHAIN, ACC_ERROR, ACC_ABORT, ACC_TICKET, ACC_DONE, ACC_WORDS = 8 };
 
+// The output pointers the kernels use: vr_outputs without the queue (which only kernel C of vr_dyn3.cuh and the
+// closing kernel write).  Kept apart from the ABI struct on purpose: the 80-register tile kernel's allocation is
+// sensitive to the parameter layout (8 more bytes here cost it 16 bytes of spills and 1.5 % of the headline).
+struct RunOut {
+    int32_t* d_batch_round_off;
+    int32_t* d_round_uid_off;
+    int32_t* d_round_prims;
+    uint32_t* d_unique_ids;
+    uint16_t* d_assembly_map;
+    float* d_shaded4;
+    uint32_t* d_shaded_attr;
+    int32_t* d_shade_counts;
+    int64_t* d_stats;
+    int64_t cap_unique;
+    int64_t cap_rounds;
+};
+
 struct RunCtx {
     const uint32_t* __restrict__ idx;
     int64_t n_idx;
@@ -55,7 +72,7 @@ struct RunCtx {
     int n_fused_tiles;
     int n_state_words;  // words of tile_state to clear: the tiles, and for the tile kernel its group tables behind them
     // outputs
-    vr_outputs out;
+    RunOut out;
 };
 
 // First failing batch wins, as in the reference's in-order loop (strategies.py:470):
@@ -2003,7 +2020,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     c.tile_state = (unsigned long long*)(ws + L.tile_state);
     c.stage_uid = (uint32_t*)(ws + L.stage_uid);
     c.stage_round = (uint32_t*)(ws + L.stage_round);
-    c.out = *out;
+    c.out = RunOut{out->d_batch_round_off, out->d_round_uid_off, out->d_round_prims, out->d_unique_ids, out->d_assembly_map,
+                   out->d_shaded4, out->d_shaded_attr, out->d_shade_counts, out->d_stats, out->cap_unique, out->cap_rounds};
     ShaderParams sp{};
     if (shader) {
         sp.kind = shader->kind; sp.has_matrix = shader->has_matrix;
@@ -2050,6 +2068,7 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     Dyn3Plan d3 = dyn3_plan(strategy, cfg, hc, max_span, c.enforce_budget != 0, shader, out);
     if (!allow_fuse || nb == 0 || nb >= (1 << 30)) d3.ok = false;
     d3.g.aux = ws + L.aux;
+    d3.g.queue = out->d_stream_xyz;
     d3.g.prefetch = debug_knobs().dyn3_prefetch;
     c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, kDyn3Tile) : 0;
     g_prof_marks = 0;
