@@ -477,10 +477,12 @@ def main():
             f_steps = max(5, min(steps, 20))
             t_form = timed_steps(form, f_steps)[0] / f_steps
 
-            def whole():
-                o = engine.dynamic_offsets_device(d_idx, cfg, workspace=ws_form)
-                engine.run_device(wl["strategy"], d_idx, o[:-1], o[1:], o.numel() - 1, n_idx, max_span, cfg, hcfg, spec,
-                                  buffers=bufs)
+            def whole():  # no host round trip: the batch count stays on the device (vr_run_counted)
+                o, cnt = engine.dynamic_offsets_device(d_idx, cfg, workspace=ws_form, sync=False)
+                return engine.run_device(wl["strategy"], d_idx, None, None, 0, 0, max_span, cfg, hcfg, spec, buffers=bufs,
+                                         counted=(o, cnt))
+            chk = whole().check()
+            assert (chk.n_batches, chk.invocations) == (nb, inv), "formation + stage without the host in between differs"
             whole()
             t_whole = timed_steps(whole, f_steps)[0] / f_steps
             alg_w = alg + 4 * n_idx

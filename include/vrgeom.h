@@ -241,6 +241,21 @@ int vr_run(int strategy, const uint32_t *d_indices, int64_t n_indices, const int
            const vr_batch_config *cfg, const vr_hash_config *hcfg, const vr_shader *shader,
            const vr_outputs *out, void *d_workspace, size_t workspace_bytes, void *stream);
 
+/* Batch formation -> stage with NO host round trip: the batch count stays on the device.
+ *   d_offsets, d_n_batches   as written by vr_dynamic_batches / vr_dynamic_batches_draws on the same stream
+ *                            (d_n_batches: int64[2] = {count, vr_status}; a non-zero status is reported through the
+ *                            statistics block, as is a count above n_batches_max);
+ *   n_batches_max            upper bound the launch, the outputs and the workspace are sized for:
+ *                            vr_dynamic_batch_bound(n_indices, cfg, n_draws) -- every batch but the last of a draw holds
+ *                            at least min(max_unique - ps + 1, max_primitives * ps) indices (batching.py:106-118).
+ * Outputs as vr_run with contiguous batches; VR_STAT_BATCHES and the closing table entries use the device count.
+ * Implemented by the three-kernel sort / hash / phash path (budgeted batches): VR_ERR_UNSUPPORTED otherwise. */
+int64_t vr_dynamic_batch_bound(int64_t n_indices, const vr_batch_config *cfg, int32_t n_draws);
+int vr_run_counted(int strategy, const uint32_t *d_indices, int64_t n_indices, const int32_t *d_offsets,
+                   int64_t n_batches_max, const int64_t *d_n_batches, int32_t max_span,
+                   const vr_batch_config *cfg, const vr_hash_config *hcfg, const vr_shader *shader,
+                   const vr_outputs *out, void *d_workspace, size_t workspace_bytes, void *stream);
+
 /* strategies.py:456-463 + :132-152: expanded per-corner record stream,
  * out[slot] = shaded[round base + assembly_map[slot]].  d_stream_pos3 is float[3*n_slots]
  * (TriangleStream.as_array() for the position shader), d_stream_ids uint32[n_slots]

@@ -108,6 +108,10 @@ _SIGNATURES = {
     "vr_run": (C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                          C.c_int32, C.POINTER(BatchConfigC), C.POINTER(HashConfigC), C.POINTER(ShaderC),
                          C.POINTER(OutputsC), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "vr_dynamic_batch_bound": (C.c_int64, [C.c_int64, C.POINTER(BatchConfigC), C.c_int32]),
+    "vr_run_counted": (C.c_int, [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int32,
+                                 C.POINTER(BatchConfigC), C.POINTER(HashConfigC), C.POINTER(ShaderC), C.POINTER(OutputsC),
+                                 C.c_void_p, C.c_size_t, C.c_void_p]),
     "vr_profile_enable": (C.c_int, [C.c_int]),
     "vr_last_launch_count": (C.c_int, []),
     "vr_last_kernel_path": (C.c_int, []),

@@ -41,7 +41,17 @@ struct Dyn3Geom {
     int prefetch;        // kernel C: L2 prefetch of the distinct vertices before they are put in order
     unsigned char* aux;  // hash/phash: per batch occupancy bitmap[32 B] | home[span'] | slot[span'] | grp u16[span']
     float* queue;        // vr_outputs.d_stream_xyz (kernel C with QUEUE)
+    const int64_t* nb_dev;  // vr_run_counted: device int64[2] = {batch count, vr_status} of vr_dynamic_batches, or NULL
 };
+
+// vr_run_counted: the batch count lives on the device (the output of vr_dynamic_batches, no host round trip); the
+// launch was sized for an upper bound.  A failed batch formation leaves no batches.
+__device__ __forceinline__ int dyn3_batch_count(const RunCtx& c, const Dyn3Geom& g) {
+    if (!g.nb_dev) return c.n_batches;
+    if (__ldg(g.nb_dev + 1) != 0) return 0;
+    const long long n = __ldg(g.nb_dev);
+    return (int)(n < 0 ? 0 : n > c.n_batches ? c.n_batches : n);
+}
 
 __device__ __forceinline__ int64_t dyn3_aux_base(const RunCtx& c, int b, int mo) { return ((int64_t)mo * 4 + (int64_t)b * 128) & ~15LL; }
 __device__ __forceinline__ int dyn3_aux_stride(int span) { return (span + 15) & ~15; }
@@ -53,7 +63,9 @@ constexpr int kDyn3AuxHome = 32;  // byte offset of home[] behind the bitmap
 // a shuffled mesh (~255 indices) the 40+ registers cost more resident warps than that saves (measured), so vr_run picks
 // the variant by the average batch length.
 template <bool ORDERED, bool PHASH, bool WIDE>
-__global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, Dyn3Geom g) {
+__global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c_in, Dyn3Geom g) {
+    RunCtx c = c_in;
+    c.n_batches = dyn3_batch_count(c_in, g);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_tile;
     __shared__ int2 s_cnt[kDyn3Tile];
@@ -61,6 +73,11 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c, D
     if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long*)&c.acc[ACC_TICKET], 1ull);  // tiles in ticket order
     __syncthreads();
     const int tile = s_tile;
+    if (g.nb_dev && tile == 0 && threadIdx.x == 0) {  // what the host would have checked before the launch
+        const long long fst = __ldg(g.nb_dev + 1), fnb = __ldg(g.nb_dev);
+        if (fst != 0) report_error(c, 0, (int)fst);
+        else if (fnb > c_in.n_batches) report_error(c, 0, VR_ERR_CAPACITY);
+    }
     const bool abort = c.acc[ACC_ABORT] != 0;
     unsigned char* base = smem_raw + (size_t)wid * g.per_warp_bytes;
     uint32_t* kkey = reinterpret_cast<uint32_t*>(base);  // [q] the set
@@ -280,7 +297,9 @@ struct Dyn3Bitmap {
 };
 
 template <bool PHASH>
-__global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertThreads) dyn3_insert_kernel(RunCtx c, Dyn3Geom g) {
+__global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertThreads) dyn3_insert_kernel(RunCtx c_in, Dyn3Geom g) {
+    RunCtx c = c_in;
+    c.n_batches = dyn3_batch_count(c_in, g);
     constexpr int NT = PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertThreads;
     __shared__ uint32_t s_bm[8 * NT];
     __shared__ unsigned char s_dd[PHASH ? 64 * NT : 1];  // deferred ids of the open group (d)
@@ -421,7 +440,9 @@ __device__ __forceinline__ void warp_bitonic_blocked(uint32_t (&v)[R], int lane)
 // QUEUE: also write the stage's output queue (vr_outputs.d_stream_xyz) -- a separate instantiation, so that the
 // default kernel's register allocation does not pay for it
 template <int STRATEGY, bool QUEUE>
-__global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx c, ShaderParams sp, Dyn3Geom g) {
+__global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx c_in, ShaderParams sp, Dyn3Geom g) {
+    RunCtx c = c_in;
+    c.n_batches = dyn3_batch_count(c_in, g);
     __shared__ __align__(16) uint32_t s_list[kDyn3Warps][256];  // the round's unique ids, in output order
     __shared__ __align__(16) uint16_t s_of_d[kDyn3Warps][256];  // per distinct id d: distance home -> slot << 8 | position in the list
     __shared__ uint32_t s_bm[kDyn3Warps][16];                   // hash: occupancy words, their exclusive popcount prefix

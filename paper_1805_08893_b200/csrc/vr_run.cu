@@ -1967,9 +1967,10 @@ size_t vr_run_workspace_bytes(int strategy, int64_t span_total, int64_t nb, cons
     return ws_layout(strategy, span_total, nb, cfg).total;
 }
 
-int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_bbegin, const int32_t* d_bend,
-           int64_t nb, int64_t span_total, int32_t max_span, const vr_batch_config* cfg, const vr_hash_config* hcfg,
-           const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_) {
+static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_bbegin, const int32_t* d_bend,
+                    int64_t nb, int64_t span_total, int32_t max_span, const vr_batch_config* cfg, const vr_hash_config* hcfg,
+                    const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_,
+                    const int64_t* d_n_batches) {
     const bool no_budget = (strategy & VR_FLAG_NO_BUDGET) != 0;
     const bool static_batches = (strategy & VR_FLAG_STATIC) != 0;
     const bool allow_fuse = (strategy & VR_FLAG_NO_FUSE) == 0;
@@ -2069,6 +2070,8 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     if (!allow_fuse || nb == 0 || nb >= (1 << 30)) d3.ok = false;
     d3.g.aux = ws + L.aux;
     d3.g.queue = out->d_stream_xyz;
+    d3.g.nb_dev = d_n_batches;
+    if (d_n_batches && !d3.ok) return VR_ERR_UNSUPPORTED;  // (the device-side batch count is implemented by the three-kernel path)
     d3.g.prefetch = debug_knobs().dyn3_prefetch;
     c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, kDyn3Tile) : 0;
     g_prof_marks = 0;
@@ -2223,6 +2226,33 @@ int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_
     g_last_launches = (nb > 0 ? 3 : 1) + ((!contiguous && nb > 0) ? 1 : 0) + (L.n_scan_tiles ? 3 : 1) + closing_queue();
     VR_CUDA_CHECK(cudaGetLastError());
     return VR_OK;
+}
+
+int vr_run(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_bbegin, const int32_t* d_bend,
+           int64_t nb, int64_t span_total, int32_t max_span, const vr_batch_config* cfg, const vr_hash_config* hcfg,
+           const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_) {
+    return run_impl(strategy, d_idx, n_idx, d_bbegin, d_bend, nb, span_total, max_span, cfg, hcfg, shader, out, d_ws, ws_bytes, stream_, nullptr);
+}
+
+int64_t vr_dynamic_batch_bound(int64_t n, const vr_batch_config* cfg, int32_t n_draws) {
+    if (vr_check_batch_config(cfg) || n <= 0) return 0;
+    // batching.py:106-118: a batch closes because the next primitive would not fit, i.e. it holds more than
+    // max_unique - ps distinct ids (so at least that many indices) or max_primitives primitives; only the last batch of
+    // a draw may be shorter
+    const int64_t ps = cfg->primitive_size;
+    int64_t by_unique = (int64_t)cfg->max_unique - ps + 1;
+    if (by_unique < ps) by_unique = ps;
+    const int64_t by_cap = (cfg->max_indices / ps) * ps;
+    const int64_t shortest = by_unique < by_cap ? by_unique : by_cap;
+    return n / (shortest > 0 ? shortest : 1) + (n_draws > 0 ? n_draws : 1) + 1;
+}
+
+int vr_run_counted(int strategy, const uint32_t* d_idx, int64_t n_idx, const int32_t* d_offsets, int64_t nb_max,
+                   const int64_t* d_n_batches, int32_t max_span, const vr_batch_config* cfg, const vr_hash_config* hcfg,
+                   const vr_shader* shader, const vr_outputs* out, void* d_ws, size_t ws_bytes, void* stream_) {
+    if (!d_n_batches || !d_offsets || nb_max <= 0) return VR_ERR_BAD_CONFIG;
+    return run_impl((strategy & ~0xF00) | VR_FLAG_CONTIGUOUS | (strategy & VR_FLAG_NO_BUDGET), d_idx, n_idx, d_offsets, d_offsets + 1, nb_max,
+                    n_idx, max_span, cfg, hcfg, shader, out, d_ws, ws_bytes, stream_, d_n_batches);
 }
 
 int vr_last_launch_count(void) { return g_last_launches; }

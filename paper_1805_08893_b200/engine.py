@@ -109,8 +109,12 @@ def static_offsets_device(index_count: int, cfg: BatchConfig, device=None) -> to
     return offs
 
 
-def dynamic_offsets_device(indices, cfg: BatchConfig, device=None, workspace=None) -> torch.Tensor:
-    """batching.py:87-125 on the GPU -> int32 offsets (length n_batches+1; length 0 if empty)."""
+def dynamic_offsets_device(indices, cfg: BatchConfig, device=None, workspace=None, sync: bool = True):
+    """batching.py:87-125 on the GPU -> int32 offsets (length n_batches+1; length 0 if empty).
+
+    sync=False: no host round trip -- returns (offsets at full capacity, counts) where counts is the device int64[2]
+    {batch count, vr_status} of vr_dynamic_batches; hand both to run_device(..., counted=(offsets, counts)), which
+    launches for the upper bound vr_dynamic_batch_bound and lets the kernels read the count (vr_run_counted)."""
     lib = N.require_cuda()
     d_idx = to_device_indices(indices, device)
     dev = d_idx.device
@@ -129,6 +133,8 @@ def dynamic_offsets_device(indices, cfg: BatchConfig, device=None, workspace=Non
     with torch.cuda.device(dev):
         raise_status(lib.vr_dynamic_batches(_ptr(d_idx), n, C.byref(c), _ptr(offs), _ptr(nb),
                                             _ptr(workspace), ws_bytes, _stream_ptr()))
+    if not sync:
+        return offs, nb
     nbh = nb.cpu()
     if int(nbh[1]) != 0:
         raise_status(int(nbh[1]))
@@ -163,6 +169,7 @@ class DeviceRun:
         self.launches = 0
         self.kernel_path = 0
         self.stream_xyz = None  # the output queue, when the run was asked for it (want_queue)
+        self._counted = False   # launched through vr_run_counted: n_batches is an upper bound until the statistics are read
         self._stats = None
 
     def relaunch(self) -> "DeviceRun":
@@ -171,7 +178,7 @@ class DeviceRun:
         if self.shade_counts is not None:
             self.shade_counts.zero_()
         with torch.cuda.device(self._device):
-            st = lib.vr_run(*self._args, _stream_ptr())
+            st = (lib.vr_run_counted if self._counted else lib.vr_run)(*self._args, _stream_ptr())
         raise_status(st)
         self._stats = None
         self.launches = lib.vr_last_launch_count()  # kernels this call launched (bench.py's gpu_launches)
@@ -186,6 +193,8 @@ class DeviceRun:
 
     def check(self):
         """Raise what the reference would have raised for the first failing batch."""
+        if self._counted:  # the true batch count arrives with the statistics block
+            self.n_batches = int(self.stats()[N.VR_STAT_BATCHES])
         err = int(self.stats()[N.VR_STAT_ERROR])
         if err != -1:
             raise_status(err & 0xFF, err >> 8)
@@ -315,7 +324,7 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
                shader: ShaderSpec | None = None, *, want_counts: bool = False,
                buffers: RunBuffers | None = None, enforce_budget: bool = True,
                contiguous: bool | None = None, static: bool = False, fuse: bool = True,
-               want_queue: bool = False, plan_only: bool = False) -> DeviceRun:
+               want_queue: bool = False, counted=None, plan_only: bool = False) -> DeviceRun:
     """vr_run on the current stream.  No host synchronisation; call .check()/.flat() to read back.
     `plan_only` prepares buffers and arguments without launching: `.relaunch()` then issues the same
     run again (same inputs, outputs overwritten) at the cost of one C call, for callers that repeat a
@@ -325,6 +334,13 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         raise ConfigError(f"unknown strategy {strategy!r}; expected one of {tuple(N.STRATEGY_IDS)}")
     sid = N.STRATEGY_IDS[strategy]
     dev = d_indices.device
+    if counted is not None:
+        # (offsets at full capacity, device batch count) straight from dynamic_offsets_device(sync=False): sized for the
+        # upper bound, the kernels read the count (vr_run_counted); d_begin / d_end / n_batches / span_total are derived
+        c_offs, c_counts = counted
+        n_batches = int(lib.vr_dynamic_batch_bound(d_indices.numel(), C.byref(_cfg_c(cfg)), 0))
+        n_batches = min(n_batches, int(c_offs.numel()) - 1)
+        d_begin, d_end, span_total, contiguous = c_offs[:-1], c_offs[1:], int(d_indices.numel()), True
     if contiguous is None:  # begin/end are two views of one offsets array
         contiguous = (n_batches > 0 and d_begin.data_ptr() + 4 == d_end.data_ptr()
                       and d_begin.is_contiguous() and d_end.is_contiguous())
@@ -383,9 +399,14 @@ def run_device(strategy: str, d_indices: torch.Tensor, d_begin: torch.Tensor, d_
         run.shade_counts.data_ptr() if run.shade_counts is not None else None,
         run.stats_dev.data_ptr(), max_inv.value, max_rounds.value,
         run.stream_xyz.data_ptr() if run.stream_xyz is not None else None)
-    args = (sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
-            span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws), ws.numel())
-    run._keep = (ws, shader, c, h, sh, out, d_indices, d_begin, d_end)
+    if counted is not None:
+        args = (sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(counted[0]), n_batches, _ptr(counted[1]), max_span,
+                C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws), ws.numel())
+        run._counted = True
+    else:
+        args = (sid | flags, _ptr(d_indices), d_indices.numel(), _ptr(d_begin), _ptr(d_end), n_batches,
+                span_total, max_span, C.byref(c), hp, C.byref(sh), C.byref(out), _ptr(ws), ws.numel())
+    run._keep = (ws, shader, c, h, sh, out, d_indices, d_begin, d_end, counted)
     run._args, run._device = args, dev
     if plan_only:
         return run

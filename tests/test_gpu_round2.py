@@ -239,3 +239,36 @@ def test_sharded_run_with_exchanged_boundaries(cuda_lib):
     b, plan_b = shard.run_sharded("hash", d_idx, cfg, hc, spec, batching="dynamic", rank=0, world=1)
     assert (plan_a.batch_lo, plan_a.batch_hi, plan_a.index_lo, plan_a.index_hi) == (plan_b.batch_lo, plan_b.batch_hi, plan_b.index_lo, plan_b.index_hi)
     assert_flat_equal(a.flat(), b.flat(), "exchange vs whole-stream scan")
+
+
+@pytest.mark.parametrize("strategy", ["sort", "hash", "phash"])
+def test_formation_to_stage_without_host_round_trip(cuda_lib, strategy):
+    """vr_dynamic_batches -> vr_run_counted: the batch count stays on the device (the launch is sized for
+    vr_dynamic_batch_bound); results, statistics and error reporting equal the synchronous path."""
+    import ctypes as C
+    cfg, hc = BatchConfig(), HashConfig()
+    lib = N.require_cuda()
+    for mesh in (P.gen_grid(140, 90), P.shuffle_triangles(P.gen_grid(120, 77), 5), P.gen_icosphere(4)):
+        d_idx = engine.to_device_indices(mesh.indices)
+        spec = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions),
+                                 matrix=MATRIX, vertex_count=mesh.vertex_count)
+        offs = engine.dynamic_offsets_device(d_idx, cfg)
+        want = engine.run_device(strategy, d_idx, offs[:-1], offs[1:], offs.numel() - 1, len(mesh.indices), 1023, cfg, hc, spec,
+                                 want_counts=True)
+        full, counts = engine.dynamic_offsets_device(d_idx, cfg, sync=False)
+        bound = lib.vr_dynamic_batch_bound(len(mesh.indices), C.byref(engine._cfg_c(cfg)), 0)
+        assert bound >= offs.numel() - 1
+        run = engine.run_device(strategy, d_idx, None, None, 0, 0, 1023, cfg, hc, spec, want_counts=True, counted=(full, counts))
+        assert run.kernel_path == 4
+        got, ref = run.flat(), want.flat()
+        assert run.n_batches == want.n_batches == offs.numel() - 1
+        assert_flat_equal(got, ref, strategy)
+        assert np.array_equal(got["shaded"], ref["shaded"]) and np.array_equal(got["shade_counts"], ref["shade_counts"])
+        assert np.array_equal(run.stats()[:7], want.stats()[:7]) and run.probes == want.probes
+    # the smallest budget: one triangle per batch, the bound is exact
+    idx = np.array([0, 1, 2, 3, 3, 3, 4, 5, 6], dtype=np.uint32)
+    tiny = BatchConfig(max_unique=3, max_indices=6, primitive_size=3)
+    full, counts = engine.dynamic_offsets_device(idx, tiny, sync=False)
+    run = engine.run_device(strategy, engine.to_device_indices(idx), None, None, 0, 0, 6, tiny, HashConfig(table_size=4),
+                            engine.ShaderSpec(kind=N.VR_SHADER_IDENTITY, vertex_count=7), counted=(full, counts))
+    assert run.flat()["round_prims"].tolist() == [1, 1, 1] and run.n_batches == 3
