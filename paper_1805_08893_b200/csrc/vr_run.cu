@@ -2103,6 +2103,11 @@ static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const in
             prof_mark(stream);
             prof_mark(stream);
             const size_t csmem = want_queue ? (size_t)kDyn3Warps * (256 * sizeof(float4) + 96 * sizeof(float)) : 0;  // the batch's shaded records + a row of the queue
+            if (want_queue) {  // (static + dynamic shared memory is within 512 bytes of the 48 KB default: opt in explicitly)
+                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_finish_kernel<VR_SORT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_finish_kernel<VR_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+                VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_finish_kernel<VR_PHASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+            }
             switch (strategy * 2 + (want_queue ? 1 : 0)) {
             case VR_SORT * 2: dyn3_finish_kernel<VR_SORT, false><<<ftiles, kDyn3Warps * 32, 0, stream>>>(c, sp, d3.g); break;
             case VR_SORT * 2 + 1: dyn3_finish_kernel<VR_SORT, true><<<ftiles, kDyn3Warps * 32, csmem, stream>>>(c, sp, d3.g); break;
