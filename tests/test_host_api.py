@@ -231,3 +231,38 @@ def test_oracle_draws_helper_concatenates_per_mesh_runs():
     assert list(got["flat"]["round_uid_off"]) == [0, fa.invocations, fa.invocations + fb.invocations]
     assert got["per_draw"] == [(1, fa.invocations), (1, fb.invocations)]
     assert got["totals"]["invocations"] == fa.invocations + fb.invocations
+
+
+def test_round2_entry_points_validate_without_a_device():
+    """Host-side checks of the round-2 entry points (no compute: every one of them refuses or answers before it would
+    touch a GPU)."""
+    lib = _native.lib()
+    cfg = _native.BatchConfigC(96, 256, 1023, 32, 256, 3)
+    # every batch but the last holds >= min(max_unique - ps + 1, max_primitives * ps) indices (batching.py:106-118)
+    assert lib.vr_dynamic_batch_bound(21591654, ctypes.byref(cfg), 0) == 21591654 // 254 + 2
+    assert lib.vr_dynamic_batch_bound(21591654, ctypes.byref(cfg), 1000) == 21591654 // 254 + 1001
+    one = _native.BatchConfigC(96, 256, 1023, 32, 256, 1)
+    assert lib.vr_dynamic_batch_bound(300000, ctypes.byref(one), 0) == 300000 // 256 + 2
+    assert lib.vr_dynamic_batch_bound(0, ctypes.byref(cfg), 0) == 0
+    # ranges of the stream are whole groups of 64 chunks of max(1024, max_primitives) primitives
+    assert lib.vr_dynamic_group_indices(ctypes.byref(cfg)) == 1024 * 64 * 3
+    assert lib.vr_dynamic_group_count(21591654, ctypes.byref(cfg)) == -(-(-(-7197218 // 1024)) // 64)
+    assert lib.vr_dynamic_table_words(21591654, ctypes.byref(cfg)) == 2 * (1023 // 3)
+    # cache model: cache.py:85-86 alignment, cache.py:36-40 validation
+    cc = _native.CacheConfigC(28, 1024, 256, 3)
+    assert lib.vr_cache_workspace_bytes(9000, ctypes.byref(cc)) > 0
+    assert lib.vr_cache_workspace_bytes(9001, ctypes.byref(cc)) == 0
+    out = (ctypes.c_int64 * 4)()
+    assert lib.vr_simulate_cache(None, 9001, ctypes.byref(cc), 0, None, out, None, 0, None) == _native.VR_ERR_UNALIGNED
+    assert lib.vr_simulate_cache(None, 9000, ctypes.byref(_native.CacheConfigC(0, 1024, 256, 3)), 0, None, out, None, 0, None) \
+        == _native.VR_ERR_BAD_CONFIG
+    # walk client: walk.py:62-70 validation, device limit of 1024 candidate moves
+    wc = _native.WalkConfigC()
+    wc.grid_w, wc.grid_h, wc.max_move_distance, wc.kept_moves, wc.n_gaussians = 1, 256, 16, 8, 0
+    st = (ctypes.c_int64 * 1)()
+    assert lib.vr_walk_likelihoods(None, 0, ctypes.byref(wc), None, st, None) == _native.VR_ERR_BAD_CONFIG
+    wc.grid_w, wc.max_move_distance = 256, 19
+    assert lib.vr_walk_likelihoods(None, 0, ctypes.byref(wc), None, st, None) == _native.VR_ERR_UNSUPPORTED
+    wc.max_move_distance, wc.kept_moves = 1, 6  # 5 candidate moves within distance 1
+    assert lib.vr_walk_likelihoods(None, 0, ctypes.byref(wc), None, st, None) == _native.VR_ERR_BAD_CONFIG
+    assert lib.vr_debug_reload_knobs() == 0
