@@ -47,6 +47,16 @@ for r in range(3):
 g = torch.stack(tabs)
 for r in range(3):
     shard.dynamic_offsets_exchange(d_big, cfg, r, 3, gather=lambda t: g, workspace=wss[r])
+# formation -> stage without the host (vr_run_counted) and the in-stage output queue
+for strat in ("sort", "hash", "phash"):
+    full, counts = engine.dynamic_offsets_device(mesh.indices, cfg, sync=False)
+    spec_m = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(mesh.positions), matrix=M, vertex_count=mesh.vertex_count)
+    engine.run_device(strat, engine.to_device_indices(mesh.indices), None, None, 0, 0, 1023, cfg, HashConfig(), spec_m, counted=(full, counts), want_queue=True).check()
+offs_g = engine.static_offsets_device(len(grid.indices), cfg)
+spec_g = engine.ShaderSpec(kind=N.VR_SHADER_POSITION, positions4=engine.to_device_positions4(grid.positions), matrix=M, vertex_count=grid.vertex_count)
+engine.run_device("warp", engine.to_device_indices(grid.indices), offs_g[:-1], offs_g[1:], offs_g.numel() - 1, len(grid.indices), 96, cfg, None, spec_g, static=True, want_queue=True).check()
+r = engine.run_device("naive", engine.to_device_indices(grid.indices), offs_g[:-1], offs_g[1:], offs_g.numel() - 1, len(grid.indices), 96, cfg, None, spec_g, want_queue=True).check()
+r.assembly_map_u8(); r.shaded_xyz()
 P.ideal_report(mesh)
 P.simulate_parallel_cache(mesh.indices, P.CacheConfig(num_processors=3, wave_width=96, entries=64), miss_counts=np.zeros(mesh.vertex_count, dtype=np.int64))
 P.run_walk(P.WalkConfig(grid=(40, 40), agents=500, max_move_distance=5, kept_moves=4, steps=2), "hash", BatchConfig(primitive_size=1, batch_size=576))
