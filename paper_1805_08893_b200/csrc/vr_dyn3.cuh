@@ -10,8 +10,8 @@
 //   A  one WARP per batch: the batch's distinct ids by insertion into a private open-addressing set
 //      (shared memory, CAS), numbered d = 0.. -- in first-occurrence order for hash/phash, which is the
 //      reference's insertion order.  Leaves d of every element in the assembly map (rewritten by C), the
-//      distinct ids and (hash/phash) their home slots in the workspace, (rounds, uniques) per batch; the
-//      CTA's tail turns these into output offsets with a decoupled look-back over CTA tiles.
+//      distinct ids and (hash/phash) their home slots in the workspace, (rounds, uniques) per batch, the batch's
+//      output offset inside its 32-batch tile and the tile's totals; the last tile to finish scans the totals.
 //   B  hash/phash only, one THREAD per batch: the reference's sequential table construction replayed
 //      on the DISTINCT ids only.  Duplicates never change the table, and "probe until the slot is free"
 //      is a find-next-zero on an occupancy bitmap, so a batch costs <= 256 short steps; all batches of
@@ -28,7 +28,7 @@
 #pragma once
 
 constexpr int kDyn3Warps = 8;          // warps per CTA of kernels A and C
-constexpr int kDyn3Tile = 32;          // batches per CTA of kernel A (one look-back per tile)
+constexpr int kDyn3Tile = 32;          // batches per CTA of kernel A (one entry of the offset scan per tile)
 constexpr int kDyn3InsertThreads = 128;  // batches per CTA of kernel B (hash); phash keeps more per batch: half of that
 
 struct Dyn3Geom {
@@ -57,22 +57,63 @@ __device__ __forceinline__ int64_t dyn3_aux_base(const RunCtx& c, int b, int mo)
 __device__ __forceinline__ int dyn3_aux_stride(int span) { return (span + 15) & ~15; }
 constexpr int kDyn3AuxHome = 32;  // byte offset of home[] behind the bitmap
 
+// Output offsets without a scan pass and without any tile waiting for another: kernel A leaves, per batch, the
+// (rounds, ids) of the batches before it in its TILE (32 batches), per tile its totals, and adds the tile's totals to
+// its GROUP (32 tiles) and its SUPERGROUP (32 groups = 32768 batches).  Kernel C adds up, per batch, the supergroups
+// before its own, the groups of its supergroup before its own, the tiles of its group before its own (one word per
+// lane each) and the batch's offset in its tile.  Words are rounds << 32 | ids; ids sum to <= the index count < 2^31
+// and rounds to <= the batch count < 2^30, so the halves never carry.
+constexpr int kDyn3Group = 32;
+struct Dyn3Levels {
+    unsigned long long* tiles;   // [n_tiles]
+    unsigned long long* groups;  // [n_groups]
+    unsigned long long* supers;  // [n_supers]
+    int n_supers;
+};
+__host__ __device__ __forceinline__ int dyn3_state_words(int n_tiles) {
+    const int n_groups = (n_tiles + kDyn3Group - 1) / kDyn3Group;
+    return n_tiles + 1 + n_groups + 1 + (n_groups + kDyn3Group - 1) / kDyn3Group + 1;
+}
+__device__ __forceinline__ Dyn3Levels dyn3_levels(const RunCtx& c) {
+    const int n_tiles = c.n_fused_tiles, n_groups = (n_tiles + kDyn3Group - 1) / kDyn3Group;
+    Dyn3Levels l;
+    l.tiles = c.tile_state;
+    l.groups = l.tiles + n_tiles + 1;
+    l.supers = l.groups + n_groups + 1;
+    l.n_supers = (n_groups + kDyn3Group - 1) / kDyn3Group;
+    return l;
+}
+__device__ __forceinline__ int2 dyn3_offsets(const RunCtx& c, int b, int lane) {
+    const Dyn3Levels l = dyn3_levels(c);
+    const int tile = b / kDyn3Tile, grp = tile / kDyn3Group, sup = grp / kDyn3Group;
+    unsigned long long w = lane < tile % kDyn3Group ? __ldcg(l.tiles + grp * kDyn3Group + lane) : 0ull;
+    w += lane < grp % kDyn3Group ? __ldcg(l.groups + sup * kDyn3Group + lane) : 0ull;
+    for (int k = lane; k < sup; k += 32) w += __ldcg(l.supers + k);
+    const int2 in_tile = c.seg_off[b];
+    return make_int2(in_tile.x + (int)__reduce_add_sync(0xffffffffu, (unsigned)(w >> 32)),
+                     in_tile.y + (int)__reduce_add_sync(0xffffffffu, (unsigned)(w & 0xFFFFFFFFull)));
+}
+// (rounds, ids) of the whole run: one thread, after every tile of kernel A has finished
+__device__ __forceinline__ int2 dyn3_totals(const RunCtx& c) {
+    const Dyn3Levels l = dyn3_levels(c);
+    unsigned long long w = 0;
+    for (int k = 0; k < l.n_supers; k++) w += __ldcg(l.supers + k);
+    return make_int2((int)(w >> 32), (int)(w & 0xFFFFFFFFull));
+}
+
 // ---- A ------------------------------------------------------------------------------------------
 // WIDE: 64 elements per step, two per lane, their two probe chains interleaved -- for LONG batches (a strip-ordered mesh:
 // ~760 indices per batch): the second chain hides the first one's shared-memory atomic latency.  On the short batches of
 // a shuffled mesh (~255 indices) the 40+ registers cost more resident warps than that saves (measured), so vr_run picks
 // the variant by the average batch length.
 template <bool ORDERED, bool PHASH, bool WIDE>
-__global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c_in, Dyn3Geom g) {
+__global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kernel(RunCtx c_in, Dyn3Geom g) {
     RunCtx c = c_in;
     c.n_batches = dyn3_batch_count(c_in, g);
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ int s_tile;
     __shared__ int2 s_cnt[kDyn3Tile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_tile = (int)atomicAdd((unsigned long long*)&c.acc[ACC_TICKET], 1ull);  // tiles in ticket order
-    __syncthreads();
-    const int tile = s_tile;
+    const int tile = (int)blockIdx.x;
     if (g.nb_dev && tile == 0 && threadIdx.x == 0) {  // what the host would have checked before the launch
         const long long fst = __ldg(g.nb_dev + 1), fnb = __ldg(g.nb_dev);
         if (fst != 0) report_error(c, 0, (int)fst);
@@ -219,53 +260,20 @@ __global__ void __launch_bounds__(kDyn3Warps * 32) dyn3_dedup_kernel(RunCtx c_in
         }
     }
     __syncthreads();
-    // ---- output offsets: decoupled look-back over tiles (every predecessor holds an earlier ticket, so it is
-    // resident or finished)
+    // ---- output offsets: see dyn3_offsets.  (A decoupled look-back here kept the CTA's shared memory and warp slots
+    // occupied while one warp polled its predecessors: measured ~1/3 of a CTA's residency when the grid runs in waves.)
     if (wid == 0) {
         const int2 v = s_cnt[lane];
         const int ir = warp_incl_scan(v.x, lane), iu = warp_incl_scan(v.y, lane);
-        const long long ar = __shfl_sync(0xffffffffu, ir, 31), au = __shfl_sync(0xffffffffu, iu, 31);
-        unsigned long long* __restrict__ state = c.tile_state;
-        if (lane == 0)
-            st_relaxed_gpu_u64(state + tile, (tile == 0 ? kStateInclusive : kStateAggregate) | ((unsigned long long)ar << 32) | (unsigned long long)au);
-        long long er = 0, eu = 0;
-        bool lost = false;
-        if (tile > 0) {
-            for (int pz = tile - 1;; pz -= 32) {
-                const int idx = pz - lane;
-                unsigned long long word = kStateInclusive;  // before the first tile: inclusive zero
-                int spins = 0;
-                for (;;) {
-                    if (idx >= 0) word = ld_relaxed_gpu_u64(state + idx);
-                    if (__all_sync(0xffffffffu, (word >> 62) != 0)) break;
-                    __nanosleep(64);  // the predecessors are busy deduplicating: leave them the issue slots
-                    if (++spins > (1 << 12)) __nanosleep(500);  // (a preempted producer is not a lost one: ~0.5 s before giving up)
-                    if (spins > (1 << 20)) { lost = true; break; }
-                }
-                if (lost) break;
-                const uint32_t incl = __ballot_sync(0xffffffffu, (word >> 62) == 2);
-                const int upto = incl ? __ffs((int)incl) - 1 : 31;
-                if (lane <= upto) {
-                    er += (long long)((word >> 32) & 0x3FFFFFFFull);
-                    eu += (long long)(word & 0xFFFFFFFFull);
-                }
-                if (incl) break;
-            }
-#pragma unroll
-            for (int d = 16; d > 0; d >>= 1) {
-                er += __shfl_xor_sync(0xffffffffu, er, d);
-                eu += __shfl_xor_sync(0xffffffffu, eu, d);
-            }
-            if (lane == 0) {
-                if (lost) report_error(c, (int64_t)tile * kDyn3Tile, VR_ERR_CUDA);
-                st_relaxed_gpu_u64(state + tile, kStateInclusive | ((unsigned long long)((er + ar) & 0x3FFFFFFF) << 32) | (unsigned long long)((eu + au) & 0xFFFFFFFFll));
-            }
-        }
         const int bl = tile * kDyn3Tile + lane;
-        if (bl < c.n_batches)
-            c.seg_off[bl] = make_int2((int)min(er + ir - v.x, 0x7fffffffLL), (int)min(eu + iu - v.y, 0x7fffffffLL));
-        if (lane == 0 && (tile + 1) * kDyn3Tile >= c.n_batches)
-            c.seg_off[c.n_batches] = make_int2((int)min(er + ar, 0x7fffffffLL), (int)min(eu + au, 0x7fffffffLL));
+        if (bl < c.n_batches) c.seg_off[bl] = make_int2(ir - v.x, iu - v.y);
+        if (lane == 31) {
+            const Dyn3Levels l = dyn3_levels(c);
+            const unsigned long long total = ((unsigned long long)(uint32_t)ir << 32) | (unsigned long long)(uint32_t)iu;
+            l.tiles[tile] = total;
+            atomicAdd(l.groups + tile / kDyn3Group, total);
+            atomicAdd(l.supers + tile / (kDyn3Group * kDyn3Group), total);
+        }
     }
 }
 
@@ -454,7 +462,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
     float* qstage = QUEUE ? reinterpret_cast<float*>(smem_raw) + 4 * 256 * kDyn3Warps + 96 * wid : nullptr;  // one row of records
     if (b < c.n_batches && !c.acc[ACC_ABORT]) {
         const int2 cnt = c.counts[b];
-        const int2 off = c.seg_off[b];
+        const int2 off = dyn3_offsets(c, b, lane);
         const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
         if (lane == 0 && c.out.d_batch_round_off) c.out.d_batch_round_off[b] = off.x;
         const int nu = cnt.y;
@@ -615,9 +623,17 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
                 if (lane + 32 * k < n) element(lane + 32 * k, early[k]);
                 if (QUEUE && 32 * k < n) queue_row(32 * k);
             }
-            for (int i0 = 32 * EA; i0 < n; i0 += 32) {
-                if (i0 + lane < n) element(i0 + lane, amap[i0 + lane]);
-                if (QUEUE) queue_row(i0);
+            // longer batches: EA steps' numbers in flight together (a load per step would be a dependent L2 round trip per
+            // step: the stores to the same array keep the compiler from hoisting it)
+            for (int c0 = 32 * EA; c0 < n; c0 += 32 * EA) {
+#pragma unroll
+                for (int k = 0; k < EA; k++) early[k] = c0 + lane + 32 * k < n ? (uint32_t)__ldcg(amap + c0 + lane + 32 * k) : 0u;
+#pragma unroll
+                for (int k = 0; k < EA; k++) {
+                    if (c0 + 32 * k >= n) break;  // uniform
+                    if (c0 + lane + 32 * k < n) element(c0 + lane + 32 * k, early[k]);
+                    if (QUEUE) queue_row(c0 + 32 * k);
+                }
             }
             if (STRATEGY != VR_SORT) {
                 fast = __reduce_add_sync(0xffffffffu, fast);
@@ -639,7 +655,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
         const unsigned long long done = atomicAdd((unsigned long long*)&c.acc[ACC_DONE], 1ull);
         if (done == (unsigned long long)gridDim.x - 1) {
             __threadfence();
-            const int2 tot = __ldcg(c.seg_off + c.n_batches);
+            const int2 tot = dyn3_totals(c);
             finish_stats(c, tot.x, tot.y);
         }
     }

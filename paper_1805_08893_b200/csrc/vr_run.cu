@@ -1789,7 +1789,7 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.acc = o; o += align_up(ACC_WORDS * 8);
     // kRowThreads tiles (>= kFastThreads tiles) + the tile kernel's two group tables (one group = 32 tiles)
     // (and the kDyn3Warps-batch tiles of the three-kernel sort/hash path)
-    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 8) + 1 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);
+    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 8) + 8 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);  // (>= dyn3_state_words(nb / 32))
     L.stage_uid = o;
     if (strategy != VR_NAIVE) {
         size_t words = (size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64;
@@ -2077,7 +2077,8 @@ static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const in
     g_prof_marks = 0;
     g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : d3.ok ? 4 : 0;
     prof_mark(stream);
-    c.n_state_words = rows ? c.n_fused_tiles + 1 + 2 * ((int)ceil_div(c.n_fused_tiles, kRowGroup) + 1) : c.n_fused_tiles;
+    c.n_state_words = rows ? c.n_fused_tiles + 1 + 2 * ((int)ceil_div(c.n_fused_tiles, kRowGroup) + 1)
+                      : d3.ok ? dyn3_state_words(c.n_fused_tiles) : c.n_fused_tiles;
     init_kernel<<<(int)ceil_div(c.n_state_words + ACC_WORDS, 256), 256, 0, stream>>>(c);
     if (!contiguous && nb > 0) span_scan_kernel<<<1, 1024, 0, stream>>>(c);
     prof_mark(stream);

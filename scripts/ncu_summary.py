@@ -23,10 +23,10 @@ def main(path):
         for i, h in enumerate(hdr):
             if h in WANT:
                 print(f'  {h:70s} {r[i]:>18s} {units[i]}')
-            if 'warp_issue_stalled' in h and h.endswith('_per_warp_active.pct'):
-                try: stalls.append((float(r[i]), h.split('stalled_')[1].replace('_per_warp_active.pct', '')))
+            if h.startswith('smsp__average_warps_issue_stalled_') and h.endswith('_per_issue_active.ratio'):
+                try: stalls.append((float(r[i]), h.split('stalled_')[1].replace('_per_issue_active.ratio', '')))
                 except ValueError: pass
-        print('  top stalls (% of warp-active cycles):', ', '.join(f'{n} {v:.0f}' for v, n in sorted(stalls, reverse=True)[:6]))
+        print('  top stalls (warps stalled per issued instruction):', ', '.join(f'{n} {v:.2f}' for v, n in sorted(stalls, reverse=True)[:7]))
 if __name__ == '__main__':
     for p in sys.argv[1:]:
         main(p)
