@@ -353,8 +353,11 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
     c.n_batches = dyn3_batch_count(c_in, g);
     constexpr int NT = PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertThreads;
     __shared__ uint32_t s_bm[8 * NT];
-    __shared__ unsigned char s_dd[PHASH ? 64 * NT : 1];  // deferred ids of the open group (d)
-    __shared__ unsigned char s_dh[PHASH ? 64 * NT : 1];  //   and their home slots
+    // phash: deferred ids of the open group (d) and their home slots, [w][NT] each -- dynamic, so that a narrower group
+    // width leaves room for more resident batches (w = 32: 10 CTAs/SM instead of 8)
+    extern __shared__ unsigned char s_deferred[];
+    unsigned char* s_dd = s_deferred;
+    unsigned char* s_dh = s_deferred + (PHASH ? g.w * NT : 0);
     __shared__ unsigned char s_slot[PHASH ? 256 * NT : 1];  // slot of every d (written out of order)
     const int t = threadIdx.x;
     const int b = blockIdx.x * NT + t;

@@ -2100,7 +2100,8 @@ static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const in
             else st = launch_a(dyn3_dedup_kernel<true, true, false>);
             if (st) return st;
             if (strategy == VR_HASH) dyn3_insert_kernel<false><<<(int)ceil_div(nb, kDyn3InsertThreads), kDyn3InsertThreads, 0, stream>>>(c, d3.g);
-            if (strategy == VR_PHASH) dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads / 2), kDyn3InsertThreads / 2, 0, stream>>>(c, d3.g);
+            if (strategy == VR_PHASH)
+                dyn3_insert_kernel<true><<<(int)ceil_div(nb, kDyn3InsertThreads / 2), kDyn3InsertThreads / 2, (size_t)2 * cfg->warp_width * (kDyn3InsertThreads / 2), stream>>>(c, d3.g);
             prof_mark(stream);
             prof_mark(stream);
             const size_t csmem = want_queue ? (size_t)kDyn3Warps * (256 * sizeof(float4) + 96 * sizeof(float)) : 0;  // the batch's shaded records + a row of the queue
