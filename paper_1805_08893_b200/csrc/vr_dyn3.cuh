@@ -83,37 +83,7 @@ __device__ __forceinline__ Dyn3Levels dyn3_levels(const RunCtx& c) {
     l.n_supers = (n_groups + kDyn3Group - 1) / kDyn3Group;
     return l;
 }
-// Kernel C of the hash strategy runs PERSISTENT warps: a warp takes every (warps of the grid)-th batch, and everything a
-// batch's work starts from -- its counts, offset in its tile, range, vertex base and the three rows of sums above -- is
-// copied for the NEXT batch into a per-warp shared-memory header by cp.async while the current batch is processed: a
-// warp that takes one batch and exits spends a fifth of its life waiting for these loads (ncu).  The loop costs ~12
-// registers; measured on the 7 M-triangle meshes it pays for hash (-4..8 %: the slot / home-slot loads make its start
-// the longest) at 4 CTAs/SM, not for sort (the sorting network wants the registers and the warps: +6 %) and is neutral
-// for phash, which both keep the one-batch form.
-constexpr int kDyn3HdrWords = 4 + 3 * 32;  // u64: counts | seg_off | begin,end | vbase,- | tiles[32] | groups[32] | supers[32]
-__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, bool take) {  // !take: zero fill, nothing read
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem), "r"(take ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cp_async_4(void* smem, const void* gmem, bool take) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem), "r"(take ? 4 : 0) : "memory");
-}
-__device__ __forceinline__ void dyn3_fetch_header(const RunCtx& c, const ShaderParams& sp, int b, unsigned long long* hdr, int lane) {
-    if (b < c.n_batches) {
-        const Dyn3Levels l = dyn3_levels(c);
-        const int tile = b / kDyn3Tile, grp = tile / kDyn3Group, sup = grp / kDyn3Group;
-        if (lane == 0) cp_async_8(hdr + 0, c.counts + b, true);
-        if (lane == 1) cp_async_8(hdr + 1, c.seg_off + b, true);
-        if (lane == 2) cp_async_4(reinterpret_cast<int*>(hdr + 2), c.bbegin + b, true);
-        if (lane == 3) cp_async_4(reinterpret_cast<int*>(hdr + 2) + 1, c.bend + b, true);
-        if (lane == 4) cp_async_4(reinterpret_cast<int*>(hdr + 3), sp.batch_base ? sp.batch_base + b : c.bbegin, sp.batch_base != nullptr);
-        cp_async_8(hdr + 4 + lane, l.tiles + grp * kDyn3Group + (lane < tile % kDyn3Group ? lane : 0), lane < tile % kDyn3Group);
-        cp_async_8(hdr + 36 + lane, l.groups + sup * kDyn3Group + (lane < grp % kDyn3Group ? lane : 0), lane < grp % kDyn3Group);
-        cp_async_8(hdr + 68 + lane, l.supers + (lane < sup ? lane : 0), lane < sup);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-}
-// (one batch per warp: the same sums by direct loads)
-__device__ __forceinline__ int2 dyn3_offsets_direct(const RunCtx& c, int b, int lane) {
+__device__ __forceinline__ int2 dyn3_offsets(const RunCtx& c, int b, int lane) {
     const Dyn3Levels l = dyn3_levels(c);
     const int tile = b / kDyn3Tile, grp = tile / kDyn3Group, sup = grp / kDyn3Group;
     unsigned long long w = lane < tile % kDyn3Group ? __ldcg(l.tiles + grp * kDyn3Group + lane) : 0ull;
@@ -122,18 +92,6 @@ __device__ __forceinline__ int2 dyn3_offsets_direct(const RunCtx& c, int b, int 
     const int2 in_tile = c.seg_off[b];
     return make_int2(in_tile.x + (int)__reduce_add_sync(0xffffffffu, (unsigned)(w >> 32)),
                      in_tile.y + (int)__reduce_add_sync(0xffffffffu, (unsigned)(w & 0xFFFFFFFFull)));
-}
-// the batch's output offsets from its header (supergroups past the 32nd -- more than a million batches -- read directly)
-__device__ __forceinline__ int2 dyn3_offsets(const RunCtx& c, int b, const unsigned long long* hdr, int lane) {
-    unsigned long long w = hdr[4 + lane] + hdr[36 + lane] + hdr[68 + lane];
-    const int sup = b / (kDyn3Tile * kDyn3Group * kDyn3Group);
-    if (sup > 32) {
-        const Dyn3Levels l = dyn3_levels(c);
-        for (int k = 32 + lane; k < sup; k += 32) w += __ldcg(l.supers + k);
-    }
-    const unsigned long long in_tile = hdr[1];  // int2: x = rounds (low word), y = ids
-    return make_int2((int)(in_tile & 0xFFFFFFFFull) + (int)__reduce_add_sync(0xffffffffu, (unsigned)(w >> 32)),
-                     (int)(in_tile >> 32) + (int)__reduce_add_sync(0xffffffffu, (unsigned)(w & 0xFFFFFFFFull)));
 }
 // (rounds, ids) of the whole run: one thread, after every tile of kernel A has finished
 __device__ __forceinline__ int2 dyn3_totals(const RunCtx& c) {
@@ -493,45 +451,26 @@ __device__ __forceinline__ void warp_bitonic_blocked(uint32_t (&v)[R], int lane)
 
 // QUEUE: also write the stage's output queue (vr_outputs.d_stream_xyz) -- a separate instantiation, so that the
 // default kernel's register allocation does not pay for it
-__host__ __device__ constexpr bool dyn3_finish_persistent(int strategy) { return strategy == VR_HASH; }
 template <int STRATEGY, bool QUEUE>
-__global__ void __launch_bounds__(kDyn3Warps * 32, dyn3_finish_persistent(STRATEGY) ? 4 : 5) dyn3_finish_kernel(RunCtx c_in, ShaderParams sp, Dyn3Geom g) {
-    constexpr bool PERSIST = dyn3_finish_persistent(STRATEGY);
+__global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx c_in, ShaderParams sp, Dyn3Geom g) {
     RunCtx c = c_in;
     c.n_batches = dyn3_batch_count(c_in, g);
     __shared__ __align__(16) uint32_t s_list[kDyn3Warps][256];  // the round's unique ids, in output order
     __shared__ __align__(16) uint16_t s_of_d[kDyn3Warps][256];  // per distinct id d: distance home -> slot << 8 | position in the list
     __shared__ uint32_t s_bm[kDyn3Warps][16];                   // hash: occupancy words, their exclusive popcount prefix
     extern __shared__ __align__(16) unsigned char smem_raw[];   // the batch's shaded records [warp][256] when the queue is wanted
-    __shared__ __align__(16) unsigned long long s_hdr[PERSIST ? kDyn3Warps : 1][2][PERSIST ? kDyn3HdrWords : 1];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     float* __restrict__ queue = QUEUE ? g.queue : nullptr;
     float4* kept = QUEUE ? reinterpret_cast<float4*>(smem_raw) + 256 * wid : nullptr;
     float* qstage = QUEUE ? reinterpret_cast<float*>(smem_raw) + 4 * 256 * kDyn3Warps + 96 * wid : nullptr;  // one row of records
-    const int total_warps = (int)gridDim.x * kDyn3Warps;
-    int b = c.acc[ACC_ABORT] != 0 ? c.n_batches : (int)blockIdx.x * kDyn3Warps + wid;
-    int buf = 0;
-    if (PERSIST) dyn3_fetch_header(c, sp, b, s_hdr[PERSIST ? wid : 0][0], lane);
-    while (b < c.n_batches) {
-        int2 cnt, off;
-        int begin, n, vbase;
-        if (PERSIST) {
-            dyn3_fetch_header(c, sp, b + total_warps, s_hdr[PERSIST ? wid : 0][buf ^ 1], lane);
-            asm volatile("cp.async.wait_group 1;" ::: "memory");  // this batch's header (every lane waits for its own copies)
-            __syncwarp();
-            const unsigned long long* hdr = s_hdr[PERSIST ? wid : 0][buf];
-            cnt = make_int2((int)(hdr[0] & 0xFFFFFFFFull), (int)(hdr[0] >> 32));
-            off = dyn3_offsets(c, b, hdr, lane);
-            begin = (int)(hdr[2] & 0xFFFFFFFFull);
-            n = (int)(hdr[2] >> 32) - begin;
-            vbase = (int)(hdr[3] & 0xFFFFFFFFull);
-        } else {
-            cnt = c.counts[b];
-            off = dyn3_offsets_direct(c, b, lane);
-            begin = __ldg(c.bbegin + b);
-            n = __ldg(c.bend + b) - begin;
-            vbase = sp.batch_base ? __ldg(sp.batch_base + b) : 0;
-        }
+    __shared__ unsigned int s_fast[kDyn3Warps], s_slow[kDyn3Warps], s_cmax[kDyn3Warps];  // the warps' probe statistics
+    if (lane == 0) { s_fast[wid] = 0; s_slow[wid] = 0; s_cmax[wid] = 0; }
+    const int b = blockIdx.x * kDyn3Warps + wid;
+    if (b < c.n_batches && !c.acc[ACC_ABORT]) {
+        const int2 cnt = c.counts[b];
+        const int2 off = dyn3_offsets(c, b, lane);
+        const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
+        const int vbase = sp.batch_base ? __ldg(sp.batch_base + b) : 0;
         if (lane == 0 && c.out.d_batch_round_off) c.out.d_batch_round_off[b] = off.x;
         const int nu = cnt.y;
         const bool fits = (int64_t)off.y + nu <= c.out.cap_unique && (int64_t)off.x + cnt.x <= c.out.cap_rounds;
@@ -706,23 +645,30 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, dyn3_finish_persistent(STRATE
                 fast = __reduce_add_sync(0xffffffffu, fast);
                 slow = __reduce_add_sync(0xffffffffu, slow);
                 cmax = __reduce_max_sync(0xffffffffu, cmax);
-                if (lane == 0) {
-                    atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], (unsigned long long)fast);
-                    if (STRATEGY == VR_PHASH) atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_SLOW], (unsigned long long)slow);
-                    atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)cmax);
+                if (lane == 0) {  // (added up per CTA below: an atomic per batch on the same three addresses serialises in L2)
+                    s_fast[wid] = fast;
+                    s_slow[wid] = slow;
+                    s_cmax[wid] = cmax;
                 }
             }
             if (!QUEUE) shade_stream<VR_SORT>(c, sp, list, nu, off.y, lane, 32, mo, vbase, b);
         }
-        if (!PERSIST) break;
-        __syncwarp();  // the warp's lists and the header buffer are free
-        b += total_warps;
-        buf ^= 1;
     }
-    if (PERSIST) asm volatile("cp.async.wait_group 0;" ::: "memory");
     // the last CTA to finish writes the statistics block (every CTA's probe counts are in by then)
     __syncthreads();
     if (threadIdx.x == 0) {
+        if (STRATEGY != VR_SORT) {
+            unsigned long long fast = 0, slow = 0;
+            unsigned int cmax = 0;
+            for (int k = 0; k < kDyn3Warps; k++) {
+                fast += s_fast[k];
+                slow += s_slow[k];
+                cmax = max(cmax, s_cmax[k]);
+            }
+            if (fast) atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_FAST], fast);
+            if (slow) atomicAdd((unsigned long long*)&c.acc[ACC_PROBES_SLOW], slow);
+            if (cmax) atomicMax(&c.acc[ACC_MAX_CHAIN], (long long)cmax);
+        }
         __threadfence();
         const unsigned long long done = atomicAdd((unsigned long long*)&c.acc[ACC_DONE], 1ull);
         if (done == (unsigned long long)gridDim.x - 1) {

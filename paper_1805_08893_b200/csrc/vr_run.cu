@@ -2110,19 +2110,7 @@ static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const in
                 VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_finish_kernel<VR_HASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
                 VR_CUDA_CHECK(cudaFuncSetAttribute(dyn3_finish_kernel<VR_PHASH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
             }
-            // hash: persistent warps, one CTA per slot of the GPU (see dyn3_fetch_header); else one batch per warp
-            auto launch_c = [&](auto kernel) -> int {
-                int grid = ftiles;
-                if (dyn3_finish_persistent(strategy)) {
-                    int dev = 0, sms = 148, per_sm = 1;
-                    cudaGetDevice(&dev);
-                    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kDyn3Warps * 32, csmem) != cudaSuccess || per_sm < 1) per_sm = 1;
-                    if (grid > sms * per_sm) grid = sms * per_sm;
-                }
-                kernel<<<grid, kDyn3Warps * 32, csmem, stream>>>(c, sp, d3.g);
-                return VR_OK;
-            };
+            auto launch_c = [&](auto kernel) { kernel<<<ftiles, kDyn3Warps * 32, csmem, stream>>>(c, sp, d3.g); };
             switch (strategy * 2 + (want_queue ? 1 : 0)) {
             case VR_SORT * 2: launch_c(dyn3_finish_kernel<VR_SORT, false>); break;
             case VR_SORT * 2 + 1: launch_c(dyn3_finish_kernel<VR_SORT, true>); break;
