@@ -101,6 +101,12 @@ __device__ __forceinline__ int2 dyn3_totals(const RunCtx& c) {
     return make_int2((int)(w >> 32), (int)(w & 0xFFFFFFFFull));
 }
 
+__device__ __forceinline__ uint32_t atomicCAS_shared(uint32_t saddr, uint32_t cmp, uint32_t val) {
+    uint32_t r;
+    asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(r) : "r"(saddr), "r"(cmp), "r"(val) : "memory");
+    return r;
+}
+
 // ---- A ------------------------------------------------------------------------------------------
 // WIDE: 64 elements per step, two per lane, their two probe chains interleaved -- for LONG batches (a strip-ordered mesh:
 // ~760 indices per batch): the second chain hides the first one's shared-memory atomic latency.  On the short batches of
@@ -126,6 +132,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
     // position of the id, so later atomicMin's leave it alone); else u16 [q] number d of the id
     uint32_t* kpos = kkey + g.q;
     uint16_t* kidx = reinterpret_cast<uint16_t*>(kpos);
+    const uint32_t a_keys = (uint32_t)__cvta_generic_to_shared(kkey);
+    const uint32_t a_dummy = (uint32_t)__cvta_generic_to_shared(base + g.per_warp_bytes - 128 + 4 * lane);  // one spare word per lane
     const uint32_t qmask = (uint32_t)g.q - 1;
     const int qshift = 32 - ilog2((uint32_t)g.q);
     const uint32_t lt = (1u << lane) - 1;
@@ -167,17 +175,22 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
                     uint32_t ha = (id_a * 0x9E3779B1u) >> qshift, hb = (id_b * 0x9E3779B1u) >> qshift;
                     bool first_a = false, first_b = false;
                     bool pa = va, pb = vb;
-                    while (pa || pb) {
-                        if (pa) {
-                            const uint32_t prev = atomicCAS(&kkey[ha], kEmpty, id_a);
-                            if (prev == kEmpty) first_a = true;
-                            if (prev == kEmpty || prev == id_a) pa = false; else ha = (ha + 1) & qmask;
-                        }
-                        if (pb) {
-                            const uint32_t prev = atomicCAS(&kkey[hb], kEmpty, id_b);
-                            if (prev == kEmpty) first_b = true;
-                            if (prev == kEmpty || prev == id_b) pb = false; else hb = (hb + 1) & qmask;
-                        }
+                    auto probe2 = [&]() {  // (branch-free, see the one-element loop below)
+                        uint32_t ra = atomicCAS_shared(pa ? a_keys + 4u * ha : a_dummy, kEmpty, id_a);
+                        uint32_t rb = atomicCAS_shared(pb ? a_keys + 4u * hb : a_dummy, kEmpty, id_b);
+                        ra = pa ? ra : id_a;
+                        rb = pb ? rb : id_b;
+                        first_a |= ra == kEmpty;
+                        first_b |= rb == kEmpty;
+                        pa = ra != kEmpty && ra != id_a;
+                        pb = rb != kEmpty && rb != id_b;
+                        ha = pa ? (ha + 1) & qmask : ha;
+                        hb = pb ? (hb + 1) & qmask : hb;
+                    };
+                    probe2();
+                    while (__any_sync(0xffffffffu, pa || pb)) {
+                        probe2();
+                        probe2();
                     }
                     if (ORDERED) {
                         if (va) atomicMin(&kpos[ha], (uint32_t)ia);
@@ -215,14 +228,25 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
                     if (i + 32 < n) id_next = __ldg(ids + i + 32);
                     uint32_t h = (id * 0x9E3779B1u) >> qshift;
                     bool first = false;
-                    if (valid) {
-                        for (;;) {
-                            const uint32_t prev = atomicCAS(&kkey[h], kEmpty, id);
-                            if (prev == kEmpty) first = true;
-                            if (prev == kEmpty || prev == id) break;
-                            h = (h + 1) & qmask;
+                    {
+                        // up to four probes per trip of a warp-uniform loop, each a PREDICATED atomic (no divergent branch per
+                        // probe: at a load of 1/4..1/2 some lane of the warp needs a third probe in most steps, and ncu showed
+                        // the warps of this kernel waiting on branches more than on the atomics).  A lane that is done -- or
+                        // has no element -- gets its own id back: "found".
+                        bool open = valid;
+                        auto probe = [&]() {
+                            uint32_t prev = atomicCAS_shared(open ? a_keys + 4u * h : a_dummy, kEmpty, id);
+                            prev = open ? prev : id;
+                            first |= prev == kEmpty;
+                            open = prev != kEmpty && prev != id;
+                            h = open ? (h + 1) & qmask : h;
+                        };
+                        probe();  // (a stream with much reuse mostly ends here: the id is in its home slot)
+                        while (__any_sync(0xffffffffu, open)) {
+                            probe();
+                            probe();
                         }
-                        if (ORDERED) atomicMin(&kpos[h], (uint32_t)i);
+                        if (ORDERED && valid) atomicMin(&kpos[h], (uint32_t)i);
                     }
                     if (ORDERED) {
                         // the reference inserts in batch order: among equal ids of this step the lowest position is the
@@ -704,7 +728,7 @@ static Dyn3Plan dyn3_plan(int strategy, const vr_batch_config* cfg, const vr_has
     if (g.u_bound > 256) return p;
     g.q = (int)next_pow2((uint32_t)((g.u_bound + 64) * 3 / 2 + 2));  // the set holds <= u_bound + 64 ids: load <= 2/3
     if (g.q < 128) g.q = 128;
-    g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4);
+    g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4) + 128;  // + one spare word per lane
     p.smem_a = (size_t)kDyn3Warps * g.per_warp_bytes;
     p.ok = true;
     return p;
