@@ -28,7 +28,7 @@
 #pragma once
 
 constexpr int kDyn3Warps = 8;          // warps per CTA of kernels A and C
-constexpr int kDyn3Tile = 32;          // batches per CTA of kernel A (one entry of the offset scan per tile)
+constexpr int kDyn3Tile = 32;          // most batches per CTA of kernel A (a TILE: one entry of the first level of offset sums); Dyn3Geom.tile_shift
 constexpr int kDyn3InsertThreads = 128;  // batches per CTA of kernel B (hash); phash keeps more per batch: half of that
 
 struct Dyn3Geom {
@@ -38,6 +38,7 @@ struct Dyn3Geom {
     int per_warp_bytes;  // shared memory per warp of kernel A
     int w, mfp;          // phash: group width, fast probes
     int strategy;
+    int tile_shift;      // log2 of the batches per tile: 5, or 4 / 3 for short runs (more CTAs than 1 per 32 batches)
     int prefetch;        // kernel C: L2 prefetch of the distinct vertices before they are put in order
     unsigned char* aux;  // hash/phash: per batch occupancy bitmap[32 B] | home[span'] | slot[span'] | grp u16[span']
     float* queue;        // vr_outputs.d_stream_xyz (kernel C with QUEUE)
@@ -83,9 +84,9 @@ __device__ __forceinline__ Dyn3Levels dyn3_levels(const RunCtx& c) {
     l.n_supers = (n_groups + kDyn3Group - 1) / kDyn3Group;
     return l;
 }
-__device__ __forceinline__ int2 dyn3_offsets(const RunCtx& c, int b, int lane) {
+__device__ __forceinline__ int2 dyn3_offsets(const RunCtx& c, int tile_shift, int b, int lane) {
     const Dyn3Levels l = dyn3_levels(c);
-    const int tile = b / kDyn3Tile, grp = tile / kDyn3Group, sup = grp / kDyn3Group;
+    const int tile = b >> tile_shift, grp = tile / kDyn3Group, sup = grp / kDyn3Group;
     unsigned long long w = lane < tile % kDyn3Group ? __ldcg(l.tiles + grp * kDyn3Group + lane) : 0ull;
     w += lane < grp % kDyn3Group ? __ldcg(l.groups + sup * kDyn3Group + lane) : 0ull;
     for (int k = lane; k < sup; k += 32) w += __ldcg(l.supers + k);
@@ -119,6 +120,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int2 s_cnt[kDyn3Tile];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (wid == 0) s_cnt[lane] = make_int2(0, 0);  // (slots past a short tile stay empty)
+    __syncthreads();
     const int tile = (int)blockIdx.x;
     if (g.nb_dev && tile == 0 && threadIdx.x == 0) {  // what the host would have checked before the launch
         const long long fst = __ldg(g.nb_dev + 1), fnb = __ldg(g.nb_dev);
@@ -139,9 +142,9 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
     const uint32_t lt = (1u << lane) - 1;
     const int wshift = PHASH ? ilog2((uint32_t)g.w) : 0;
 #pragma unroll 1
-    for (int k = 0; k < kDyn3Tile / kDyn3Warps; k++) {
+    for (int k = 0; k < (1 << g.tile_shift) / kDyn3Warps; k++) {
         const int slot_in_tile = k * kDyn3Warps + wid;
-        const int b = tile * kDyn3Tile + slot_in_tile;
+        const int b = (tile << g.tile_shift) + slot_in_tile;
         int rounds = 0, nu = 0;
         int begin, n;
         if (b < c.n_batches && !abort && validate_batch(c, b, begin, n)) {
@@ -290,8 +293,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
     if (wid == 0) {
         const int2 v = s_cnt[lane];
         const int ir = warp_incl_scan(v.x, lane), iu = warp_incl_scan(v.y, lane);
-        const int bl = tile * kDyn3Tile + lane;
-        if (bl < c.n_batches) c.seg_off[bl] = make_int2(ir - v.x, iu - v.y);
+        const int bl = (tile << g.tile_shift) + lane;
+        if (lane < (1 << g.tile_shift) && bl < c.n_batches) c.seg_off[bl] = make_int2(ir - v.x, iu - v.y);
         if (lane == 31) {
             const Dyn3Levels l = dyn3_levels(c);
             const unsigned long long total = ((unsigned long long)(uint32_t)ir << 32) | (unsigned long long)(uint32_t)iu;
@@ -492,7 +495,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
     const int b = blockIdx.x * kDyn3Warps + wid;
     if (b < c.n_batches && !c.acc[ACC_ABORT]) {
         const int2 cnt = c.counts[b];
-        const int2 off = dyn3_offsets(c, b, lane);
+        const int2 off = dyn3_offsets(c, g.tile_shift, b, lane);
         const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
         const int vbase = sp.batch_base ? __ldg(sp.batch_base + b) : 0;
         if (lane == 0 && c.out.d_batch_round_off) c.out.d_batch_round_off[b] = off.x;
@@ -728,6 +731,7 @@ static Dyn3Plan dyn3_plan(int strategy, const vr_batch_config* cfg, const vr_has
     if (g.u_bound > 256) return p;
     g.q = (int)next_pow2((uint32_t)((g.u_bound + 64) * 3 / 2 + 2));  // the set holds <= u_bound + 64 ids: load <= 2/3
     if (g.q < 128) g.q = 128;
+    g.tile_shift = 5;
     g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4) + 128;  // + one spare word per lane
     p.smem_a = (size_t)kDyn3Warps * g.per_warp_bytes;
     p.ok = true;

@@ -1789,7 +1789,7 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
     L.acc = o; o += align_up(ACC_WORDS * 8);
     // kRowThreads tiles (>= kFastThreads tiles) + the tile kernel's two group tables (one group = 32 tiles)
     // (and the kDyn3Warps-batch tiles of the three-kernel sort/hash path)
-    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 8) + 8 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);  // (>= dyn3_state_words(nb / 32))
+    L.tile_state = o; o += align_up((size_t)(ceil_div(nb, 8) + ceil_div(nb, 128) + 16 + 2 * (ceil_div(ceil_div(nb, 64), 32) + 1)) * 8);  // (>= dyn3_state_words(nb / 8))
     L.stage_uid = o;
     if (strategy != VR_NAIVE) {
         size_t words = (size_t)span_total * L.stage_factor + (size_t)nb * 8 + 64;
@@ -2073,7 +2073,9 @@ static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const in
     d3.g.nb_dev = d_n_batches;
     if (d_n_batches && !d3.ok) return VR_ERR_UNSUPPORTED;  // (the device-side batch count is implemented by the three-kernel path)
     d3.g.prefetch = debug_knobs().dyn3_prefetch;
-    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, kDyn3Tile) : 0;
+    // (short runs: fewer batches per CTA of the set dedup, so that the grid still covers the GPU)
+    d3.g.tile_shift = nb >= 16384 ? 5 : nb >= 4096 ? 4 : 3;
+    c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, (int64_t)1 << d3.g.tile_shift) : 0;
     g_prof_marks = 0;
     g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : d3.ok ? 4 : 0;
     prof_mark(stream);
