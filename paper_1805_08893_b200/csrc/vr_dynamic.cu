@@ -401,6 +401,52 @@ __global__ void __launch_bounds__(256) group_table_kernel(DynCtx c) {
     }
 }
 
+// B1 / B2 out of shared memory.  In the two kernels above every thread follows a chain of dependent global loads
+// (~12 batches per chunk, 64 chunk tables per group: ncu shows 48-60 warps waiting on the load per issued
+// instruction, 34 + 36 us for the 7 M-triangle stream).  Here the CTA first copies what its chains walk through --
+// the chunk's stretch of next[], the group's chunk tables -- coalesced, with all loads in flight, and the chains
+// run out of shared memory.
+__global__ void __launch_bounds__(256) chunk_table_smem_kernel(DynCtx c) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int* s_next = reinterpret_cast<int*>(smem_raw);  // [chunk] next start, relative to the chunk
+    const int k = c.k_lo + blockIdx.x;
+    const int lo = k * c.chunk, hi = min(c.T, lo + c.chunk), len = hi - lo;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < len; i += blockDim.x) s_next[i] = __ldg(c.next + lo + i) - lo;
+    __syncthreads();
+    for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
+        int s = o, cnt = 0;
+        while (s < len) { s = s_next[s]; cnt++; }
+        c.c_exit[(size_t)k * c.cap + o] = s >= len ? s - len : 0;
+        c.c_cnt[(size_t)k * c.cap + o] = cnt;
+    }
+}
+__global__ void __launch_bounds__(1024) group_table_smem_kernel(DynCtx c) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int g = c.g_lo + blockIdx.x;
+    const int k0 = g * kGroup, k1 = min(c.n_chunks, k0 + kGroup), nr = k1 - k0;
+    int* s_exit = reinterpret_cast<int*>(smem_raw);  // [nr][cap]
+    int* s_cnt = s_exit + kGroup * c.cap;
+    const int* __restrict__ ge = c.c_exit + (size_t)k0 * c.cap;
+    const int* __restrict__ gc = c.c_cnt + (size_t)k0 * c.cap;
+#pragma unroll 8
+    for (int i = threadIdx.x; i < nr * c.cap; i += blockDim.x) {
+        s_exit[i] = __ldg(ge + i);
+        s_cnt[i] = __ldg(gc + i);
+    }
+    __syncthreads();
+    for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
+        int e = o, cnt = 0;
+        for (int r = 0; r < nr; r++) {
+            const int at = r * c.cap + e;
+            cnt += s_cnt[at];
+            e = s_exit[at];
+        }
+        c.g_exit[(size_t)g * c.cap + o] = e;
+        c.g_cnt[(size_t)g * c.cap + o] = cnt;
+    }
+}
+
 // ---- ranges (multi-GPU): the range's own table = its group tables composed, for every entry offset ----
 __global__ void __launch_bounds__(256) range_table_kernel(DynCtx c) {
     for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < c.cap; o += gridDim.x * blockDim.x) {
@@ -675,8 +721,19 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
             const int run = knobs.greedy_run;
             greedy_next_kernel<<<(int)ceil_div(ceil_div(L.T, run), 128), 128, 0, stream>>>(c, run);
         }
-        if (n_chunks_r > 0) chunk_table_kernel<<<n_chunks_r, 256, 0, stream>>>(c);
-        if (n_groups_r > 0) group_table_kernel<<<n_groups_r, 256, 0, stream>>>(c);
+        const size_t ct_smem = (size_t)L.chunk * 4, gt_smem = (size_t)kGroup * L.cap * 8;
+        if (n_chunks_r > 0) {
+            if (ct_smem <= 48 * 1024 && !knobs.walk_global) chunk_table_smem_kernel<<<n_chunks_r, 256, ct_smem, stream>>>(c);
+            else chunk_table_kernel<<<n_chunks_r, 256, 0, stream>>>(c);
+        }
+        if (n_groups_r > 0) {
+            if (gt_smem <= 200 * 1024 && !knobs.walk_global) {
+                VR_CUDA_CHECK(cudaFuncSetAttribute(group_table_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gt_smem));
+                group_table_smem_kernel<<<n_groups_r, 1024, gt_smem, stream>>>(c);
+            } else {
+                group_table_kernel<<<n_groups_r, 256, 0, stream>>>(c);
+            }
+        }
         if (mode == 1) range_table_kernel<<<(int)ceil_div(L.cap, 256), 256, 0, stream>>>(c);
     }
     if (mode != 1) {
