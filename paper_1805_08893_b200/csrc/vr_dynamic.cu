@@ -70,6 +70,7 @@ struct DynCtx {
     int ranged;             // 1: offsets are written relative to the range's first batch, see vr_dynamic_range_*
     int32_t* r_table;       // [2 * cap] out: entry offset -> (exit offset, batches) of the whole range
     const int32_t* entry;   // [2] in (ranged): entry offset into the range, global number of its first batch
+    int entries_in_tables;  // 1: c_exit / c_cnt hold, per entry offset of the chunk's GROUP, the chunk's entry offset and the batches before it
 };
 
 // (the buffer starts 256-byte aligned and is padded: whole 16-byte stores)
@@ -435,10 +436,15 @@ __global__ void __launch_bounds__(1024) group_table_smem_kernel(DynCtx c) {
         s_cnt[i] = __ldg(gc + i);
     }
     __syncthreads();
+    // ... and, on the way, where a chain that enters the GROUP at offset o enters every chunk, and how many batches it
+    // has emitted by then: written over the chunk tables (nothing reads them after this kernel), so that once the
+    // group's true entry offset is known (B3) a chunk's entry is one look-up instead of a walk (B4)
     for (int o = threadIdx.x; o < c.cap; o += blockDim.x) {
         int e = o, cnt = 0;
         for (int r = 0; r < nr; r++) {
             const int at = r * c.cap + e;
+            c.c_exit[(size_t)(k0 + r) * c.cap + o] = e;
+            c.c_cnt[(size_t)(k0 + r) * c.cap + o] = cnt;
             cnt += s_cnt[at];
             e = s_exit[at];
         }
@@ -573,7 +579,16 @@ __global__ void __launch_bounds__(128) emit_offsets_kernel(DynCtx c) {
     const int k = c.k_lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= c.k_hi) return;
     const int lo = k * c.chunk, hi = min(c.T, lo + c.chunk);
-    int s = lo + c.c_entry[k], j = c.c_base[k] - (c.ranged ? c.entry[1] : 0);
+    int entry, base;
+    if (c.entries_in_tables) {  // (group_table_smem_kernel left every chunk's entry per group entry offset)
+        const int g = k / kGroup, eg = c.g_entry[g];
+        entry = c.c_exit[(size_t)k * c.cap + eg];
+        base = c.g_base[g] + c.c_cnt[(size_t)k * c.cap + eg];
+    } else {
+        entry = c.c_entry[k];
+        base = c.c_base[k];
+    }
+    int s = lo + entry, j = base - (c.ranged ? c.entry[1] : 0);
     while (s < hi) {
         c.offsets[j++] = s * c.ps;
         s = c.next[s];
@@ -687,6 +702,12 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
     int walk_rows = 8;
     while (walk_rows > 1 && (size_t)walk_rows * L.cap * 8 > 48 * 1024) walk_rows >>= 1;
     const bool walk_smem = (size_t)walk_rows * L.cap * 8 <= 48 * 1024 && walk_rows >= 2 && !knobs.walk_global;
+    // the walk over the groups is one CTA: as many rows at once as shared memory holds
+    int walk_rows0 = walk_rows;
+    while ((size_t)2 * walk_rows0 * L.cap * 8 <= 200 * 1024 && walk_rows0 < L.n_groups) walk_rows0 *= 2;
+    const size_t ct_smem = (size_t)L.chunk * 4, gt_smem = (size_t)kGroup * L.cap * 8;
+    const bool tables_smem = walk_smem && gt_smem <= 200 * 1024;
+    c.entries_in_tables = tables_smem ? 1 : 0;
     // (ranges are implemented by the default kernels only)
     if (mode != 0 && (!links_tile || !greedy_smem || !walk_smem || c.draw_start)) return VR_ERR_UNSUPPORTED;
     const int n_prims_r = c.s_hi - c.s_lo, n_chunks_r = c.k_hi - c.k_lo, n_groups_r = c.g_hi - c.g_lo;
@@ -721,13 +742,12 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
             const int run = knobs.greedy_run;
             greedy_next_kernel<<<(int)ceil_div(ceil_div(L.T, run), 128), 128, 0, stream>>>(c, run);
         }
-        const size_t ct_smem = (size_t)L.chunk * 4, gt_smem = (size_t)kGroup * L.cap * 8;
         if (n_chunks_r > 0) {
             if (ct_smem <= 48 * 1024 && !knobs.walk_global) chunk_table_smem_kernel<<<n_chunks_r, 256, ct_smem, stream>>>(c);
             else chunk_table_kernel<<<n_chunks_r, 256, 0, stream>>>(c);
         }
         if (n_groups_r > 0) {
-            if (gt_smem <= 200 * 1024 && !knobs.walk_global) {
+            if (tables_smem) {
                 VR_CUDA_CHECK(cudaFuncSetAttribute(group_table_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gt_smem));
                 group_table_smem_kernel<<<n_groups_r, 1024, gt_smem, stream>>>(c);
             } else {
@@ -739,10 +759,15 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
     if (mode != 1) {
         if (mode == 2) range_entry_kernel<<<1, 32, 0, stream>>>(d_tables, world, rank, L.cap, (int32_t*)(ws + L.r_entry));
         // B3 / B4: rows of 8 tables at a time through shared memory when they fit
-        if (walk_smem) table_walk_kernel<<<1, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 0, walk_rows);
-        else group_scan_kernel<<<1, 32, 0, stream>>>(c);
+        if (walk_smem) {
+            VR_CUDA_CHECK(cudaFuncSetAttribute(table_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((size_t)walk_rows0 * L.cap * 8)));
+            table_walk_kernel<<<1, 1024, (size_t)walk_rows0 * L.cap * 8, stream>>>(c, 0, walk_rows0);
+        } else {
+            group_scan_kernel<<<1, 32, 0, stream>>>(c);
+        }
         if (c.draw_start) draws_check_kernel<<<(n_draws + 256) / 256, 256, 0, stream>>>(c);
-        if (walk_smem) { if (n_groups_r > 0) table_walk_kernel<<<n_groups_r, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 1, walk_rows); }
+        if (tables_smem) { /* B4 is a look-up in emit_offsets_kernel */ }
+        else if (walk_smem) { if (n_groups_r > 0) table_walk_kernel<<<n_groups_r, 1024, (size_t)walk_rows * L.cap * 8, stream>>>(c, 1, walk_rows); }
         else chunk_entry_kernel<<<(int)ceil_div(L.n_groups, 128), 128, 0, stream>>>(c);
         if (n_chunks_r > 0) emit_offsets_kernel<<<(int)ceil_div(n_chunks_r, 128), 128, 0, stream>>>(c);
     }
