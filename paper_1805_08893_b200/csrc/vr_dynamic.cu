@@ -181,22 +181,23 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
         // double hashing over a power-of-two table (odd step)
         uint32_t h = (id * 0x9E3779B1u) >> shift;
         uint32_t step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
+        // branch-free trips: every lane issues the two atomics (a lane whose probe collided, or that is done, on a word
+        // of its own -- s_part is free until the scan), the next state is chosen by selects
+        const uint32_t a_keys = (uint32_t)__cvta_generic_to_shared(keys), a_cnt = (uint32_t)__cvta_generic_to_shared(cnt);
+        const uint32_t a_spare = (uint32_t)__cvta_generic_to_shared(&s_part[t]);
         while (__any_sync(0xffffffffu, active)) {
-            if (active) {
-                const uint32_t k = atomicCAS(&keys[h], kEmpty, id);
-                if (k == kEmpty || k == id) {
-                    slot_of[r] = (uint16_t)h;
-                    atomicAdd(&cnt[h], 1u);
-                    r += kLinkThreads;
-                    active = r < np;
-                    id = id_next;
-                    if (r + kLinkThreads < np) id_next = c.ids[hs + r + kLinkThreads];
-                    h = (id * 0x9E3779B1u) >> shift;
-                    step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
-                } else {
-                    h = (h + step) & mask;
-                }
-            }
+            uint32_t k;
+            asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(k) : "r"(active ? a_keys + 4u * h : a_spare), "r"(kEmpty), "r"(id) : "memory");
+            const bool res = active && (k == kEmpty || k == id);
+            asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(res ? a_cnt + 4u * h : a_spare) : "memory");
+            if (res) slot_of[r] = (uint16_t)h;
+            r += res ? kLinkThreads : 0;
+            const uint32_t idn = res ? id_next : id;
+            if (res && r + kLinkThreads < np) id_next = c.ids[hs + r + kLinkThreads];
+            h = res ? (idn * 0x9E3779B1u) >> shift : (h + step) & mask;
+            step = res ? ((idn * 0x85EBCA6Bu) >> shift) | 1u : step;
+            id = idn;
+            active = r < np;
         }
     }
     __syncthreads();
