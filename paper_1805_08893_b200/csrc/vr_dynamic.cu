@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(128) greedy_next_kernel(DynCtx c, int run) {
 // one batch window, coalesced, as 16-bit DISTANCES (position - prev, next - position; 65535 = none, which
 // compares like "outside any window" because a window is shorter than that), then runs the same two-pointer
 // walk out of shared memory.
+template <int PS>
 __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run, int npos_max) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint16_t* dp = reinterpret_cast<uint16_t*>(smem_raw);  // [npos_max] position - prev
@@ -326,11 +327,10 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
     }
     __syncthreads();
     const int s0 = p0 + threadIdx.x * run;
-    if (s0 >= c.s_hi) return;
-    const int s1 = min(c.s_hi, s0 + run);
+    const int s1 = s0 < c.s_hi ? min(c.s_hi, s0 + run) : s0;  // (a thread past the end stays in the warp's votes, with no starts)
     int e = s0, cnt = 0;
     int d = 0, dend = c.T;
-    if (c.draw_start) {
+    if (c.draw_start && s0 < s1) {
         int lo = 0, hi = c.n_draws;  // last d with draw_start[d] <= ps * s0
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -339,26 +339,41 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
         d = lo;
         dend = c.draw_start[d + 1] / ps;
     }
-    for (int s = s0; s < s1; s++) {
+    // The walk as a per-lane STATE MACHINE: a trip either appends primitive e to the window of start s, or closes s
+    // (next[s] = e, its indices retire) and moves to s + 1 -- both sides are computed, selects pick.  A lane makes
+    // (starts + appended primitives) trips whatever their order, so the warp makes about as many; with a loop per
+    // start the warp ran the longest inner loop among its lanes for every start (ncu: 85 M warp instructions).
+    int s = s0;
+    while (__any_sync(0xffffffffu, s < s1)) {
+        const bool live = s < s1;
         const int S = ps * s;
-        while (s >= dend) dend = c.draw_start[++d + 1] / ps;
+        if (c.draw_start) {
+            while (live && s >= dend) dend = c.draw_start[++d + 1] / ps;
+        }
         const int lim = min(dend, s + c.cap);
         if (e < s) { e = s; cnt = 0; }
-        while (e < lim) {
-            int fresh = 0;
-            for (int k = 0; k < ps; k++) {
-                const int i = ps * e + k;
-                fresh += (int)dp[i - base] > i - S;  // prev < S
-            }
-            if (e != s && cnt + fresh > c.max_unique) break;  // first primitive always accepted
-            cnt += fresh;
-            e++;
-        }
-        c.next[s] = e;
+        const bool room = live && e < lim;
+        int fresh = 0, lost = 0;
         const int E = ps * e;
-        int lost = 0;
-        for (int k = 0; k < ps; k++) lost += (int)dn[S + k - base] >= E - (S + k);  // next >= E
-        cnt -= lost;
+        if (PS == 3) {
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                const int i = E + k;
+                fresh += room && (int)dp[room ? i - base : 0] > i - S;            // prev < S
+                lost += live && (int)dn[live ? S + k - base : 0] >= E - (S + k);  // next >= E
+            }
+        } else {
+            for (int k = 0; k < ps; k++) {
+                const int i = E + k;
+                fresh += room && (int)dp[room ? i - base : 0] > i - S;
+                lost += live && (int)dn[live ? S + k - base : 0] >= E - (S + k);
+            }
+        }
+        const bool adv = room && (e == s || cnt + fresh <= c.max_unique);  // first primitive always accepted
+        if (live && !adv) c.next[s] = e;
+        cnt += adv ? fresh : -lost;
+        e += adv ? 1 : 0;
+        s += live && !adv ? 1 : 0;
     }
 }
 
@@ -736,9 +751,9 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
         // (run * ps halfwords between the lanes' streams: an odd number of 32-bit words keeps their reads on
         // different banks)
         if (greedy_smem) {
-            VR_CUDA_CHECK(cudaFuncSetAttribute(greedy_next_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(npos_s * 4)));
-            if (n_prims_r > 0)
-                greedy_next_smem_kernel<<<(int)ceil_div(n_prims_r, 128 * run_s), 128, (size_t)npos_s * 4, stream>>>(c, run_s, (int)npos_s);
+            auto kernel = c.ps == 3 ? greedy_next_smem_kernel<3> : greedy_next_smem_kernel<0>;
+            VR_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(npos_s * 4)));
+            if (n_prims_r > 0) kernel<<<(int)ceil_div(n_prims_r, 128 * run_s), 128, (size_t)npos_s * 4, stream>>>(c, run_s, (int)npos_s);
         } else {
             const int run = knobs.greedy_run;
             greedy_next_kernel<<<(int)ceil_div(ceil_div(L.T, run), 128), 128, 0, stream>>>(c, run);
