@@ -344,6 +344,45 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
     // (starts + appended primitives) trips whatever their order, so the warp makes about as many; with a loop per
     // start the warp ran the longest inner loop among its lanes for every start (ncu: 85 M warp instructions).
     int s = s0;
+    if (PS == 3) {
+        // triangles: the three distances of primitive e (to the previous occurrence) and of start s (to the next one)
+        // stay in registers; a trip reloads only the triple that moved
+        int dpv[3], dnv[3];
+#pragma unroll
+        for (int k = 0; k < 3; k++) { dpv[k] = dp[3 * s0 + k - base]; dnv[k] = dn[3 * s0 + k - base]; }
+        while (__any_sync(0xffffffffu, s < s1)) {
+            const bool live = s < s1;
+            if (c.draw_start) {
+                while (live && s >= dend) dend = c.draw_start[++d + 1] / 3;
+            }
+            const int lim = min(dend, s + c.cap);
+            if (e < s) {  // (never taken: a start's first primitive is always accepted; kept for the restatement's sake)
+                e = s; cnt = 0;
+#pragma unroll
+                for (int k = 0; k < 3; k++) dpv[k] = dp[3 * e + k - base];
+            }
+            const bool room = live && e < lim;
+            const int gap = 3 * (e - s);  // E - S
+            int fresh = 0, lost = 0;
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                fresh += room && dpv[k] > gap + k;   // prev < S
+                lost += live && dnv[k] >= gap - k;   // next >= E
+            }
+            const bool adv = room && (e == s || cnt + fresh <= c.max_unique);  // first primitive always accepted
+            if (live && !adv) c.next[s] = e;
+            cnt += adv ? fresh : -lost;
+            e += adv ? 1 : 0;
+            s += live && !adv ? 1 : 0;
+            const uint16_t* __restrict__ src = adv ? dp + (3 * e - base) : dn + (3 * s - base);
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                const int v = src[k];
+                dpv[k] = adv ? v : dpv[k];
+                dnv[k] = adv ? dnv[k] : v;
+            }
+        }
+    } else {
     while (__any_sync(0xffffffffu, s < s1)) {
         const bool live = s < s1;
         const int S = ps * s;
@@ -355,25 +394,17 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
         const bool room = live && e < lim;
         int fresh = 0, lost = 0;
         const int E = ps * e;
-        if (PS == 3) {
-#pragma unroll
-            for (int k = 0; k < 3; k++) {
-                const int i = E + k;
-                fresh += room && (int)dp[room ? i - base : 0] > i - S;            // prev < S
-                lost += live && (int)dn[live ? S + k - base : 0] >= E - (S + k);  // next >= E
-            }
-        } else {
-            for (int k = 0; k < ps; k++) {
-                const int i = E + k;
-                fresh += room && (int)dp[room ? i - base : 0] > i - S;
-                lost += live && (int)dn[live ? S + k - base : 0] >= E - (S + k);
-            }
+        for (int k = 0; k < ps; k++) {
+            const int i = E + k;
+            fresh += room && (int)dp[room ? i - base : 0] > i - S;            // prev < S
+            lost += live && (int)dn[live ? S + k - base : 0] >= E - (S + k);  // next >= E
         }
         const bool adv = room && (e == s || cnt + fresh <= c.max_unique);  // first primitive always accepted
         if (live && !adv) c.next[s] = e;
         cnt += adv ? fresh : -lost;
         e += adv ? 1 : 0;
         s += live && !adv ? 1 : 0;
+    }
     }
 }
 
