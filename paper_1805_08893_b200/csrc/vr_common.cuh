@@ -43,6 +43,7 @@ struct DebugKnobs {
     int link_tile = 2048;     // VR_LINK_TILE     batch formation: positions per tile of the link kernel
     int links_warp = 0;       // VR_LINKS_WARP    batch formation: per-warp link kernel instead of the tile kernel
     int greedy_run = 64;      // VR_GREEDY_RUN
+    int greedy_run_s = 30;    // VR_GREEDY_RUN_S   start primitives per thread of the shared-memory window walk
     int greedy_global = 0;    // VR_GREEDY_GLOBAL batch formation: windows walked in global memory
     int walk_global = 0;      // VR_WALK_GLOBAL   batch formation: chain walks in global memory
     int sort_cta = 0;         // VR_SORT_CTA      general sort path: one CTA per batch
@@ -55,7 +56,7 @@ inline DebugKnobs parse_debug_knobs() {
     DebugKnobs d;
     auto geti = [](const char* name, int& v) { if (const char* e = getenv(name)) v = atoi(e); };
     auto flag = [](const char* name, int& v) { if (getenv(name)) v = 1; };
-    geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run);
+    geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run); geti("VR_GREEDY_RUN_S", d.greedy_run_s);
     flag("VR_GREEDY_GLOBAL", d.greedy_global); flag("VR_WALK_GLOBAL", d.walk_global); flag("VR_SORT_CTA", d.sort_cta);
     geti("VR_PREFETCH", d.rows_prefetch); geti("VR_LAG", d.rows_lag); flag("VR_NO_PDL", d.no_pdl);
     geti("VR_DYN3_PREFETCH", d.dyn3_prefetch);

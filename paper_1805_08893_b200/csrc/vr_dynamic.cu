@@ -742,8 +742,8 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
     const int nslots2 = (int)next_pow2((uint32_t)(np2 + np2 / 3));  // load <= 0.75
     const size_t smem2 = (size_t)nslots2 * 4 + (size_t)(nslots2 + 1) * 4 + (size_t)np2 * 4 + 16;
     const bool links_tile = np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !knobs.links_warp;
-    int run_s = 30;
-    while ((run_s * c.ps) % 4 != 2 && run_s < 33) run_s++;
+    int run_s = knobs.greedy_run_s > 0 ? knobs.greedy_run_s : 30;
+    for (int k = 0; k < 3 && (run_s * c.ps) % 4 != 2; k++) run_s++;
     const int64_t npos_s = (int64_t)128 * run_s * c.ps + L.window + c.ps;
     const bool greedy_smem = npos_s * 4 <= 56 * 1024 && L.window < 60000 && !knobs.greedy_global;
     int walk_rows = 8;
