@@ -70,6 +70,8 @@ struct DynCtx {
     int ranged;             // 1: offsets are written relative to the range's first batch, see vr_dynamic_range_*
     int32_t* r_table;       // [2 * cap] out: entry offset -> (exit offset, batches) of the whole range
     const int32_t* entry;   // [2] in (ranged): entry offset into the range, global number of its first batch
+    int link_end;           // positions [.., link_end) have their prev[] link (n, or the range's end + one batch window)
+    int want_nxt;           // 1: the link kernels also write nxt[] (the global-memory window walk reads it; the shared-memory one derives it from prev[])
     int entries_in_tables;  // 1: c_exit / c_cnt hold, per entry offset of the chunk's GROUP, the chunk's entry offset and the batches before it
 };
 
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(128) occurrence_links_kernel(DynCtx c, int n_t
         __syncwarp();
         if (valid && i >= t0) {
             c.prev[i] = pv;
-            if (pv >= 0) c.nxt[pv] = i;
+            if (pv >= 0 && c.want_nxt) c.nxt[pv] = i;
         }
     }
 }
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
         const int i = hs + r;
         const int pva = pv >= 0 ? hs + pv : -1;
         c.prev[i] = pva;
-        if (pva >= 0) c.nxt[pva] = i;
+        if (pva >= 0 && c.want_nxt) c.nxt[pva] = i;
     }
 }
 
@@ -306,24 +308,32 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
     const int ps = c.ps;
     const int p0 = c.s_lo + blockIdx.x * blockDim.x * run;  // first start primitive of the CTA
     const int base = ps * p0;
-    const int npos = min(c.n - base, npos_max);
-    auto put = [&](int r, int pv, int nx) {
+    const int npos = min(c.link_end - base, npos_max);  // (no position past link_end is needed by a start of the range)
+    // Only prev[] is read: a position's NEXT occurrence inside the staged stretch is the position whose previous
+    // occurrence it is, so the distances to the next occurrence are scattered in shared memory (every position has at
+    // most one next occurrence: one writer per word).  A next occurrence past the staged stretch lies past every window
+    // that can hold the position, like "none".  (No nxt[] array: 86 MB less written by the link kernel -- scattered
+    // 4-byte stores --, 86 MB less read here, and no kernel to fill it with "none".)
+    for (int q = threadIdx.x; q < (npos_max + 7) / 8; q += blockDim.x)  // "none" everywhere first (16-byte stores)
+        reinterpret_cast<uint4*>(dn)[q] = make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+    __syncthreads();
+    auto put = [&](int r, int pv) {
         const int i = base + r;
-        dp[r] = (uint16_t)(pv < 0 ? 65535 : min(i - pv, 65535));
-        dn[r] = (uint16_t)(nx == kNoLink ? 65535 : min(nx - i, 65535));
+        const int dd = pv < 0 || pv >= i ? 65535 : min(i - pv, 65535);
+        dp[r] = (uint16_t)dd;
+        if (dd <= r) dn[r - dd] = (uint16_t)dd;  // (dd = 65535 > r: the stretch is shorter than that)
     };
     if ((base & 3) == 0) {  // 16-byte loads, several in flight per thread: the copy is the bulk of this kernel's traffic
         const int4* __restrict__ pv4 = reinterpret_cast<const int4*>(c.prev + base);
-        const int4* __restrict__ nx4 = reinterpret_cast<const int4*>(c.nxt + base);
         const int nq = npos >> 2;
 #pragma unroll 4
         for (int qd = threadIdx.x; qd < nq; qd += blockDim.x) {
-            const int4 a = __ldg(pv4 + qd), b = __ldg(nx4 + qd);
-            put(4 * qd, a.x, b.x); put(4 * qd + 1, a.y, b.y); put(4 * qd + 2, a.z, b.z); put(4 * qd + 3, a.w, b.w);
+            const int4 a = __ldg(pv4 + qd);
+            put(4 * qd, a.x); put(4 * qd + 1, a.y); put(4 * qd + 2, a.z); put(4 * qd + 3, a.w);
         }
-        for (int r = 4 * nq + threadIdx.x; r < npos; r += blockDim.x) put(r, c.prev[base + r], c.nxt[base + r]);
+        for (int r = 4 * nq + threadIdx.x; r < npos; r += blockDim.x) put(r, c.prev[base + r]);
     } else {
-        for (int r = threadIdx.x; r < npos; r += blockDim.x) put(r, c.prev[base + r], c.nxt[base + r]);
+        for (int r = threadIdx.x; r < npos; r += blockDim.x) put(r, c.prev[base + r]);
     }
     __syncthreads();
     const int s0 = p0 + threadIdx.x * run;
@@ -744,8 +754,9 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
     const bool links_tile = np2 <= 65535 && nslots2 <= 65535 && smem2 <= 100 * 1024 && !knobs.links_warp;
     int run_s = knobs.greedy_run_s > 0 ? knobs.greedy_run_s : 30;
     for (int k = 0; k < 3 && (run_s * c.ps) % 4 != 2; k++) run_s++;
-    const int64_t npos_s = (int64_t)128 * run_s * c.ps + L.window + c.ps;
+    const int64_t npos_s = ((int64_t)128 * run_s * c.ps + L.window + c.ps + 7) & ~(int64_t)7;  // (whole 16-byte rows of halfwords)
     const bool greedy_smem = npos_s * 4 <= 56 * 1024 && L.window < 60000 && !knobs.greedy_global;
+    c.want_nxt = greedy_smem ? 0 : 1;
     int walk_rows = 8;
     while (walk_rows > 1 && (size_t)walk_rows * L.cap * 8 > 48 * 1024) walk_rows >>= 1;
     const bool walk_smem = (size_t)walk_rows * L.cap * 8 <= 48 * 1024 && walk_rows >= 2 && !knobs.walk_global;
@@ -763,7 +774,8 @@ static int dyn_launch(int mode, const uint32_t* d_idx, int64_t n, const vr_batch
         // positions whose links are needed: the range and one batch window behind it
         const int64_t p_lo = (int64_t)c.s_lo * c.ps;
         const int64_t p_end = mode ? ((int64_t)c.s_hi * c.ps + L.window < n ? (int64_t)c.s_hi * c.ps + L.window : n) : n;
-        if (p_end > p_lo) fill_kernel<<<(int)ceil_div(ceil_div(p_end - p_lo, 4), 256), 256, 0, stream>>>(c.nxt + p_lo, (int)(p_end - p_lo), kNoLink);
+        c.link_end = (int)p_end;
+        if (p_end > p_lo && c.want_nxt) fill_kernel<<<(int)ceil_div(ceil_div(p_end - p_lo, 4), 256), 256, 0, stream>>>(c.nxt + p_lo, (int)(p_end - p_lo), kNoLink);
         const int n_tiles = (int)ceil_div(n, L.tile);
         if (links_tile) {
             // tile version: thread per position, counting sort by table slot (16-bit relative positions)
