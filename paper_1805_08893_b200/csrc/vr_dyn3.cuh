@@ -38,6 +38,7 @@ struct Dyn3Geom {
     int per_warp_bytes;  // shared memory per warp of kernel A
     int w, mfp;          // phash: group width, fast probes
     int strategy;
+    int slot_ids;        // distinct ids a batch's scratch slot holds (dyn3_slot_ids: a multiple of 16, <= 256)
     int tile_shift;      // log2 of the batches per tile: 5, or 4 / 3 for short runs (more CTAs than 1 per 32 batches)
     int prefetch;        // kernel C: L2 prefetch of the distinct vertices before they are put in order
     unsigned char* aux;  // hash/phash: per batch occupancy bitmap[32 B] | home[span'] | slot[span'] | grp u16[span']
@@ -54,9 +55,22 @@ __device__ __forceinline__ int dyn3_batch_count(const RunCtx& c, const Dyn3Geom&
     return (int)(n < 0 ? 0 : n > c.n_batches ? c.n_batches : n);
 }
 
-__device__ __forceinline__ int64_t dyn3_aux_base(const RunCtx& c, int b, int mo) { return ((int64_t)mo * 4 + (int64_t)b * 128) & ~15LL; }
-__device__ __forceinline__ int dyn3_aux_stride(int span) { return (span + 15) & ~15; }
+// Scratch of a batch at a FIXED stride by batch number (not by its place in the index buffer): kernel C issues the loads
+// of the distinct ids / slots together with the batch's header instead of behind it (one dependent round trip less in
+// a warp's life).  slot_ids = U distinct ids per batch (the configuration's largest span, at most 256, rounded up to 16):
+//   distinct ids   stage_uid + b * U                      (32-bit words)
+//   aux            aux + b * (32 + 4 U):  occupancy bitmap[32 B] | home[U] | slot[U] | grp u16[U]
+static inline int dyn3_slot_ids(const vr_batch_config* cfg) {
+    int m = cfg->max_indices > cfg->batch_size ? cfg->max_indices : cfg->batch_size;
+    if (m > 256) m = 256;
+    if (m < 16) m = 16;
+    return (m + 15) & ~15;
+}
+static inline size_t dyn3_dist_words(int64_t nb, const vr_batch_config* cfg) { return (size_t)nb * dyn3_slot_ids(cfg) + 256; }  // (+ the read-ahead of C's 8-per-lane load)
+static inline size_t dyn3_aux_bytes(int64_t nb, const vr_batch_config* cfg) { return (size_t)nb * (32 + 4 * (size_t)dyn3_slot_ids(cfg)) + 1024; }
 constexpr int kDyn3AuxHome = 32;  // byte offset of home[] behind the bitmap
+__device__ __forceinline__ int64_t dyn3_dist_base(const Dyn3Geom& g, int b) { return (int64_t)b * g.slot_ids; }
+__device__ __forceinline__ int64_t dyn3_aux_base(const Dyn3Geom& g, int b) { return (int64_t)b * (kDyn3AuxHome + 4 * g.slot_ids); }
 
 // Output offsets without a scan pass and without any tile waiting for another: kernel A leaves, per batch, the
 // (rounds, ids) of the batches before it in its TILE (32 batches), per tile its totals, and adds the tile's totals to
@@ -151,13 +165,13 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
             const int mo = batch_map_off(c, b, begin);
             const uint32_t* __restrict__ ids = c.idx + begin;
             uint16_t* __restrict__ dmap = c.out.d_assembly_map + mo;
-            uint32_t* __restrict__ dist = c.stage_uid + stage_uid_base(c, b, mo);
+            uint32_t* __restrict__ dist = c.stage_uid + dyn3_dist_base(g, b);
             if (WIDE) asm volatile("" : "+l"(dist));  // (opaque: under the 6-CTA register cap ptxas otherwise recomputes it per store)
             unsigned char* __restrict__ home = nullptr;
             uint16_t* __restrict__ grp = nullptr;
             if (ORDERED) {
-                home = g.aux + dyn3_aux_base(c, b, mo) + kDyn3AuxHome;
-                grp = reinterpret_cast<uint16_t*>(home + 2 * dyn3_aux_stride(n));
+                home = g.aux + dyn3_aux_base(g, b) + kDyn3AuxHome;
+                grp = reinterpret_cast<uint16_t*>(home + 2 * g.slot_ids);
             }
             uint32_t id_next = lane < n ? __ldg(ids + lane) : 0u;
             __syncwarp();
@@ -356,8 +370,8 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
     for (int w = 0; w < n_words; w++) s_bm[w * NT + t] = tsize >= 32 ? 0u : ~((1u << tsize) - 1u);
     const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
     const int mo = batch_map_off(c, b, begin);
-    const int stride = dyn3_aux_stride(n);
-    unsigned char* __restrict__ aux = g.aux + dyn3_aux_base(c, b, mo);
+    const int stride = g.slot_ids;
+    unsigned char* __restrict__ aux = g.aux + dyn3_aux_base(g, b);
     const unsigned char* __restrict__ home = aux + kDyn3AuxHome;
     unsigned char* __restrict__ slot = aux + kDyn3AuxHome + stride;
     const uint16_t* __restrict__ grp = reinterpret_cast<const uint16_t*>(home + 2 * stride);
@@ -494,6 +508,10 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
     if (lane == 0) { s_fast[wid] = 0; s_slow[wid] = 0; s_cmax[wid] = 0; }
     const int b = blockIdx.x * kDyn3Warps + wid;
     if (b < c.n_batches && !c.acc[ACC_ABORT]) {
+        // the batch's distinct ids in the 8-per-lane layout of a full batch: their slot depends on b alone, so the loads
+        // travel with the header's instead of behind them (smaller batches reload in their own layout below)
+        const uint4* __restrict__ dist8 = reinterpret_cast<const uint4*>(c.stage_uid + dyn3_dist_base(g, b) + 8 * lane);
+        const uint4 pre0 = __ldcg(dist8), pre1 = __ldcg(dist8 + 1);
         const int2 cnt = c.counts[b];
         const int2 off = dyn3_offsets(c, g.tile_shift, b, lane);
         const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
@@ -505,7 +523,7 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
             const int mo = batch_map_off(c, b, begin);
             uint32_t* list = s_list[wid];
             uint16_t* of_d = s_of_d[wid];
-            const uint32_t* __restrict__ dist = c.stage_uid + stage_uid_base(c, b, mo);
+            const uint32_t* __restrict__ dist = c.stage_uid + dyn3_dist_base(g, b);
             const bool want_pos = sp.kind == VR_SHADER_POSITION;
             if (lane == 0) {
                 if (c.out.d_round_uid_off) c.out.d_round_uid_off[off.x] = off.y;
@@ -521,7 +539,11 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
             auto run = [&](auto rtag) {
                 constexpr int R = decltype(rtag)::value;
                 uint32_t v[R];
-                if (R >= 4) {
+                if (R == 8) {
+                    const uint32_t w8[8] = {pre0.x, pre0.y, pre0.z, pre0.w, pre1.x, pre1.y, pre1.z, pre1.w};
+#pragma unroll
+                    for (int r = 0; r < R; r++) v[r] = lane * R + r < nu ? w8[r % 8] : 0u;
+                } else if (R >= 4) {
 #pragma unroll
                     for (int r = 0; r < R; r += 4) {
                         uint4 x = make_uint4(0, 0, 0, 0);
@@ -557,8 +579,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
                     for (int r = 0; r < R; r++)
                         if (lane * R + r < nu) of_d[v[r] & 0xFFu] = (uint16_t)(lane * R + r);
                 } else {
-                    const int stride = dyn3_aux_stride(n);
-                    const unsigned char* __restrict__ aux = g.aux + dyn3_aux_base(c, b, mo);
+                    const int stride = g.slot_ids;
+                    const unsigned char* __restrict__ aux = g.aux + dyn3_aux_base(g, b);
                     const unsigned char* __restrict__ home = aux + kDyn3AuxHome;
                     const unsigned char* __restrict__ slot = home + stride;
                     uint32_t* bm = s_bm[wid];
@@ -732,6 +754,8 @@ static Dyn3Plan dyn3_plan(int strategy, const vr_batch_config* cfg, const vr_has
     g.q = (int)next_pow2((uint32_t)((g.u_bound + 64) * 3 / 2 + 2));  // the set holds <= u_bound + 64 ids: load <= 2/3
     if (g.q < 128) g.q = 128;
     g.tile_shift = 5;
+    g.slot_ids = dyn3_slot_ids(cfg);
+    if (g.u_bound > g.slot_ids) return p;  // (a batch list with longer spans than the configuration's: the general kernels)
     g.per_warp_bytes = g.q * (strategy == VR_SORT ? 4 + 2 : 4 + 4) + 128;  // + one spare word per lane
     p.smem_a = (size_t)kDyn3Warps * g.per_warp_bytes;
     p.ok = true;

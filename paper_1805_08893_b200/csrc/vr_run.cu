@@ -1796,13 +1796,16 @@ static WsLayout ws_layout(int strategy, int64_t span_total, int64_t nb, const vr
         if (strategy == VR_WARP) {  // the tile kernel keeps its claim lists here (vr_warp_rows.cuh)
             const size_t tw = rows_scratch_words(w, cfg->batch_size, nb);
             if (tw > words) words = tw;
+        } else {  // the three-kernel path: a fixed-stride slot per batch (vr_dyn3.cuh)
+            const size_t dw = dyn3_dist_words(nb, cfg);
+            if (dw > words) words = dw;
         }
         o += align_up(words * 4);
     }
     L.stage_round = o;
     if (strategy == VR_WARP) o += align_up(((size_t)span_total / ps + nb + 64) * 4);
     L.aux = o;  // vr_dyn3.cuh: home slot / table slot / group of every distinct id
-    if (strategy == VR_HASH || strategy == VR_PHASH) o += align_up((size_t)span_total * 4 + (size_t)nb * 128 + 256);
+    if (strategy == VR_HASH || strategy == VR_PHASH) o += align_up(dyn3_aux_bytes(nb, cfg));
     L.total = o;
     return L;
 }
