@@ -511,7 +511,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, 5) dyn3_finish_kernel(RunCtx 
         // the batch's distinct ids in the 8-per-lane layout of a full batch: their slot depends on b alone, so the loads
         // travel with the header's instead of behind them (smaller batches reload in their own layout below)
         const uint4* __restrict__ dist8 = reinterpret_cast<const uint4*>(c.stage_uid + dyn3_dist_base(g, b) + 8 * lane);
-        const uint4 pre0 = __ldcg(dist8), pre1 = __ldcg(dist8 + 1);
+        uint4 pre0 = make_uint4(0, 0, 0, 0), pre1 = pre0;
+        if (c.max_span > 128) { pre0 = __ldcg(dist8); pre1 = __ldcg(dist8 + 1); }  // (only such batch lists have batches of > 128 ids)
         const int2 cnt = c.counts[b];
         const int2 off = dyn3_offsets(c, g.tile_shift, b, lane);
         const int begin = __ldg(c.bbegin + b), n = __ldg(c.bend + b) - begin;
