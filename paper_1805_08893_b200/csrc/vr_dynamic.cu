@@ -176,10 +176,12 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
     // the lane's TOTAL probes (~2 per position) rather than the sum of per-position maxima (~8 each;
     // ncu: 15 of 32 lanes active in the probe loop before).  The next position's id is loaded one ahead.
     {
-        int r = t;
-        bool active = r < np;
-        uint32_t id = active ? c.ids[hs + r] : 0u;
-        uint32_t id_next = r + kLinkThreads < np ? c.ids[hs + r + kLinkThreads] : 0u;
+        // the thread's positions t, t + 256, ...: pointers that move on when a probe resolves, a count of what is left
+        const uint32_t* __restrict__ idp = c.ids + hs + t;
+        uint16_t* slp = slot_of + t;
+        int left = t < np ? (np - t + kLinkThreads - 1) / kLinkThreads : 0;
+        uint32_t id = left > 0 ? idp[0] : 0u;
+        uint32_t id_next = left > 1 ? idp[kLinkThreads] : 0u;
         // double hashing over a power-of-two table (odd step)
         uint32_t h = (id * 0x9E3779B1u) >> shift;
         uint32_t step = ((id * 0x85EBCA6Bu) >> shift) | 1u;
@@ -187,19 +189,21 @@ __global__ void __launch_bounds__(kLinkThreads) occurrence_links_tile_kernel(Dyn
         // of its own -- s_part is free until the scan), the next state is chosen by selects
         const uint32_t a_keys = (uint32_t)__cvta_generic_to_shared(keys), a_cnt = (uint32_t)__cvta_generic_to_shared(cnt);
         const uint32_t a_spare = (uint32_t)__cvta_generic_to_shared(&s_part[t]);
-        while (__any_sync(0xffffffffu, active)) {
+        while (__any_sync(0xffffffffu, left > 0)) {
+            const bool active = left > 0;
             uint32_t k;
             asm volatile("atom.shared.cas.b32 %0, [%1], %2, %3;" : "=r"(k) : "r"(active ? a_keys + 4u * h : a_spare), "r"(kEmpty), "r"(id) : "memory");
             const bool res = active && (k == kEmpty || k == id);
             asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(res ? a_cnt + 4u * h : a_spare) : "memory");
-            if (res) slot_of[r] = (uint16_t)h;
-            r += res ? kLinkThreads : 0;
+            if (res) *slp = (uint16_t)h;
+            slp += res ? kLinkThreads : 0;
+            idp += res ? kLinkThreads : 0;
+            left -= res ? 1 : 0;
             const uint32_t idn = res ? id_next : id;
-            if (res && r + kLinkThreads < np) id_next = c.ids[hs + r + kLinkThreads];
+            if (res && left > 1) id_next = idp[kLinkThreads];
             h = res ? (idn * 0x9E3779B1u) >> shift : (h + step) & mask;
             step = res ? ((idn * 0x85EBCA6Bu) >> shift) | 1u : step;
             id = idn;
-            active = r < np;
         }
     }
     __syncthreads();
