@@ -13,7 +13,7 @@ hash / two-tier hash on the strip-ordered and on the shuffled mesh, the 1000-dra
 its own roofline fraction and -- for dynamic batches -- the figure including batch formation.
 
 N>1 (torchrun, one rank per GPU): `value` is weak scaling -- every rank runs one whole mesh (vertex buffer
-replicated), the statistics blocks are merged with one all-gather per step on a side stream.  The "sharded"
+replicated), the statistics blocks are merged with one all-gather per timed run on a side stream.  The "sharded"
 block is strong scaling: ONE configs[2] / configs[3] stream cut into whole batches per rank
 (paper_1805_08893_b200/shard.py), and the 1000-draw scene split by whole draws (LPT).
 """
