@@ -364,17 +364,14 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
         int dpv[3], dnv[3];
 #pragma unroll
         for (int k = 0; k < 3; k++) { dpv[k] = dp[3 * s0 + k - base]; dnv[k] = dn[3 * s0 + k - base]; }
-        while (__any_sync(0xffffffffu, s < s1)) {
+        // (e >= s throughout: a start's first primitive is always appended -- lim > s -- before the start can close, so
+        // the restatement's "if (e < s) restart the window" never fires and is not compiled in here)
+        auto trip = [&]() {
             const bool live = s < s1;
             if (c.draw_start) {
                 while (live && s >= dend) dend = c.draw_start[++d + 1] / 3;
             }
             const int lim = min(dend, s + c.cap);
-            if (e < s) {  // (never taken: a start's first primitive is always accepted; kept for the restatement's sake)
-                e = s; cnt = 0;
-#pragma unroll
-                for (int k = 0; k < 3; k++) dpv[k] = dp[3 * e + k - base];
-            }
             const bool room = live && e < lim;
             const int gap = 3 * (e - s);  // E - S
             int fresh = 0, lost = 0;
@@ -395,6 +392,10 @@ __global__ void __launch_bounds__(128) greedy_next_smem_kernel(DynCtx c, int run
                 dpv[k] = adv ? v : dpv[k];
                 dnv[k] = adv ? dnv[k] : v;
             }
+        };
+        while (__any_sync(0xffffffffu, s < s1)) {  // two trips per vote (a finished lane's trip changes nothing)
+            trip();
+            trip();
         }
     } else {
     while (__any_sync(0xffffffffu, s < s1)) {
