@@ -443,7 +443,7 @@ def main():
         kernel_alg = {"dedup": 4 * n_idx + 2 * n_idx + 12 * nb, "shade_finalize": 32 * inv}
         dom_name = (N.KERNEL_PATH_NAMES.get(path) if fused else None) or N.PROFILE_STAGE_NAMES[dom]
         if path == 4:  # vr_dyn3.cuh: A (+ B) are timed as 'dedup', C as 'shade_finalize'
-            dom_name = {"dedup": "dyn3 A: set dedup + look-back offsets (+ B: table replay)",
+            dom_name = {"dedup": "dyn3 A: set dedup + offset sums (+ B: table replay)",
                         "shade_finalize": "dyn3 C: ranks + local indices + shading"}.get(N.PROFILE_STAGE_NAMES[dom], dom_name)
         traffic = None  # DRAM bytes per step of the dominant kernel, from the committed ncu --set full capture
         for tf in ("r2_traffic.json", "r1_traffic.json"):
