@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(kDyn3Warps * 32, WIDE ? 6 : 0) dyn3_dedup_kern
             const uint32_t* __restrict__ ids = c.idx + begin;
             uint16_t* __restrict__ dmap = c.out.d_assembly_map + mo;
             uint32_t* __restrict__ dist = c.stage_uid + dyn3_dist_base(g, b);
-            if (WIDE) asm volatile("" : "+l"(dist));  // (opaque: under the 6-CTA register cap ptxas otherwise recomputes it per store)
+            asm volatile("" : "+l"(dist));  // (opaque: ptxas otherwise recomputes it from the kernel parameters at every store)
+            if (!WIDE) { asm volatile("" : "+l"(ids)); asm volatile("" : "+l"(dmap)); }
             unsigned char* __restrict__ home = nullptr;
             uint16_t* __restrict__ grp = nullptr;
             if (ORDERED) {
