@@ -328,20 +328,23 @@ struct Dyn3Bitmap {
     uint32_t* bm;  // + w * NT
     uint32_t all;  // one bit per word
     uint32_t full;
-    __device__ __forceinline__ uint32_t next_free(uint32_t h) const {  // first free slot at or after h, circular
+    // first free slot at or after h, circular; `held` = the word that holds it (take does not read it again)
+    __device__ __forceinline__ uint32_t next_free(uint32_t h, uint32_t& held) const {
         uint32_t w = h >> 5;
-        uint32_t bits = ~bm[w * NT] & (0xFFFFFFFFu << (h & 31));
+        held = bm[w * NT];
+        uint32_t bits = ~held & (0xFFFFFFFFu << (h & 31));
         if (bits == 0) {  // next word with a free slot, circular (w itself again last: its slots below h)
             const uint32_t open = ~full & all;
             const uint32_t above = open & ~((2u << w) - 1u);
             w = (uint32_t)__ffs((int)(above ? above : open)) - 1;
-            bits = ~bm[w * NT];
+            held = bm[w * NT];
+            bits = ~held;
         }
         return (w << 5) + (uint32_t)__ffs((int)bits) - 1;
     }
-    __device__ __forceinline__ void take(uint32_t s) {
+    __device__ __forceinline__ void take(uint32_t s, uint32_t held) {
         const uint32_t w = s >> 5;
-        const uint32_t v = bm[w * NT] | (1u << (s & 31));
+        const uint32_t v = held | (1u << (s & 31));
         bm[w * NT] = v;
         if (v == 0xFFFFFFFFu) full |= 1u << w;
     }
@@ -388,8 +391,9 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
             for (int k = 0; k < 16; k++) {
                 if (d0 + k < nu) {
                     const uint32_t h = (hw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-                    const uint32_t s = B.next_free(h);
-                    B.take(s);
+                    uint32_t held;
+                    const uint32_t s = B.next_free(h, held);
+                    B.take(s, held);
                     ow[k >> 2] |= s << (8 * (k & 3));
                 }
             }
@@ -402,8 +406,9 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
         auto flush = [&]() {  // :345: the deferred ids one at a time, from where fast probing stopped
             for (int k = 0; k < nd; k++) {
                 const uint32_t d = s_dd[k * NT + t], h = s_dh[k * NT + t];
-                const uint32_t s = B.next_free((h + mfp) & tmask);
-                B.take(s);
+                uint32_t held;
+                const uint32_t s = B.next_free((h + mfp) & tmask, held);
+                B.take(s, held);
                 s_slot[d * NT + t] = (unsigned char)s;
             }
             nd = 0;
@@ -426,9 +431,10 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
                     const int gd = (int)((gw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
                     if (gd != open_grp) { flush(); open_grp = gd; }
                     const uint32_t h = (hw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
-                    const uint32_t s = B.next_free(h);
+                    uint32_t held;
+                    const uint32_t s = B.next_free(h, held);
                     if (((s - h) & tmask) < mfp) {  // :328-339 resolved by the fast pass
-                        B.take(s);
+                        B.take(s, held);
                         s_slot[d * NT + t] = (unsigned char)s;
                     } else {
                         s_dd[nd * NT + t] = (unsigned char)d;
