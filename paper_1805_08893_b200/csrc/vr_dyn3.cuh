@@ -382,14 +382,15 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
     if (!PHASH) {
         // strategies.py:277-294 on the distinct ids: next free slot at or after the home slot
         uint4 hv = *reinterpret_cast<const uint4*>(home);
-        for (int d0 = 0; d0 < nu; d0 += 16) {
+        auto group = [&](int d0, auto whole_tag) {  // 16 ids; a whole group needs no "d < nu" per id
+            constexpr bool WHOLE = decltype(whole_tag)::value;
             const uint4 cur = hv;
             if (d0 + 16 < nu) hv = *reinterpret_cast<const uint4*>(home + d0 + 16);
             const uint32_t hw[4] = {cur.x, cur.y, cur.z, cur.w};
             uint32_t ow[4] = {0, 0, 0, 0};
 #pragma unroll
             for (int k = 0; k < 16; k++) {
-                if (d0 + k < nu) {
+                if (WHOLE || d0 + k < nu) {
                     const uint32_t h = (hw[k >> 2] >> (8 * (k & 3))) & 0xFFu;
                     uint32_t held;
                     const uint32_t s = B.next_free(h, held);
@@ -398,7 +399,10 @@ __global__ void __launch_bounds__(PHASH ? kDyn3InsertThreads / 2 : kDyn3InsertTh
                 }
             }
             *reinterpret_cast<uint4*>(slot + d0) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-        }
+        };
+        int d0 = 0;
+        for (; d0 + 16 <= nu; d0 += 16) group(d0, std::true_type{});
+        if (d0 < nu) group(d0, std::false_type{});
     } else {
         // strategies.py:321-363 on the distinct ids
         const uint32_t mfp = (uint32_t)g.mfp;
