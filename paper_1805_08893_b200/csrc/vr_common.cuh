@@ -51,6 +51,7 @@ struct DebugKnobs {
     int rows_lag = 0;         // VR_LAG           tile kernel: shade lag in tiles (0 = 1.5 x resident CTAs)
     int no_pdl = 0;           // VR_NO_PDL        no programmatic dependent launch
     int dyn3_prefetch = 0;    // VR_DYN3_PREFETCH three-kernel path: L2 prefetch of the distinct vertices before the sort
+    int dyn3_tile_shift = 0;  // VR_DYN3_TILE_SHIFT three-kernel path: log2 of the batches per CTA of the set dedup (3..5; 0 = by run length)
 };
 inline DebugKnobs parse_debug_knobs() {
     DebugKnobs d;
@@ -59,7 +60,7 @@ inline DebugKnobs parse_debug_knobs() {
     geti("VR_LINK_TILE", d.link_tile); flag("VR_LINKS_WARP", d.links_warp); geti("VR_GREEDY_RUN", d.greedy_run); geti("VR_GREEDY_RUN_S", d.greedy_run_s);
     flag("VR_GREEDY_GLOBAL", d.greedy_global); flag("VR_WALK_GLOBAL", d.walk_global); flag("VR_SORT_CTA", d.sort_cta);
     geti("VR_PREFETCH", d.rows_prefetch); geti("VR_LAG", d.rows_lag); flag("VR_NO_PDL", d.no_pdl);
-    geti("VR_DYN3_PREFETCH", d.dyn3_prefetch);
+    geti("VR_DYN3_PREFETCH", d.dyn3_prefetch); geti("VR_DYN3_TILE_SHIFT", d.dyn3_tile_shift);
     return d;
 }
 inline DebugKnobs& debug_knobs_storage() {

@@ -2078,6 +2078,7 @@ static int run_impl(int strategy, const uint32_t* d_idx, int64_t n_idx, const in
     d3.g.prefetch = debug_knobs().dyn3_prefetch;
     // (short runs: fewer batches per CTA of the set dedup, so that the grid still covers the GPU)
     d3.g.tile_shift = nb >= 16384 ? 5 : nb >= 4096 ? 4 : 3;
+    if (debug_knobs().dyn3_tile_shift >= 3 && debug_knobs().dyn3_tile_shift <= 5) d3.g.tile_shift = debug_knobs().dyn3_tile_shift;
     c.n_fused_tiles = rows ? (int)ceil_div(nb, kRowThreads) : fused ? (int)ceil_div(nb, kFastThreads) : d3.ok ? (int)ceil_div(nb, (int64_t)1 << d3.g.tile_shift) : 0;
     g_prof_marks = 0;
     g_last_path = rows ? 3 : fused ? 2 : fast_warp ? 1 : d3.ok ? 4 : 0;
