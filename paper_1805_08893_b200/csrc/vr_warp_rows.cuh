@@ -180,7 +180,10 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
     }
     // ---- E (part 1): the first U8 claims of every thread are gathered and shaded while the
     // first helper warp is still resolving the tile's output offsets
-    constexpr int U8 = 8;
+#ifndef VR_U8
+#define VR_U8 4
+#endif
+    constexpr int U8 = VR_U8;
     uint32_t uid[U8], nxt[U8];
     float4 pv[U8];
 #pragma unroll
