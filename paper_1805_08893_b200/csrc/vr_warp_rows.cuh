@@ -183,6 +183,12 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
 #ifndef VR_U8
 #define VR_U8 4
 #endif
+#ifndef VR_TRIP_UNROLL
+#define VR_TRIP_UNROLL 4  // dedup trips between two votes on "any lane still has slots"
+#endif
+#ifndef VR_HELPER_PREFETCH
+#define VR_HELPER_PREFETCH 1
+#endif
     constexpr int U8 = VR_U8;
     uint32_t uid[U8], nxt[U8];
     float4 pv[U8];
@@ -196,7 +202,7 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
             if (ht + NH * u < tot) pv[u] = __ldg(sp.pos4 + uid[u]);
 #pragma unroll
         for (int u = 0; u < U8; u++)  // the next step's vertices: on their way to L2 while this step is shaded
-            if (ht + NH * (U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
+            if (VR_HELPER_PREFETCH && ht + NH * (U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
     }
     // ---- D: output offsets of tile stile (first helper warp).  All ~600 tiles in flight reach this
     // point together, so a tile-by-tile look-back would have to walk ~600 aggregates (five dependent
@@ -211,7 +217,10 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
         const int grp = stile / kRowGroup, pos = stile % kRowGroup;
         long long pr = 0, pu = 0;  // this lane's share of the exclusive prefix of the tile
         bool found = grp == 0;
-        constexpr int LB = 2;
+#ifndef VR_LB
+#define VR_LB 2
+#endif
+        constexpr int LB = VR_LB;
         bool first = true;
         for (int pz = grp - 1; (first || (pz >= 0 && !found)) && !lost; pz -= 32 * LB) {
             unsigned long long word[LB], sum[LB], tw = 0;
@@ -306,7 +315,7 @@ __device__ __forceinline__ void rows_shade_tile(const RunCtx& c, const RowsGeom&
             if (want_pos) {
 #pragma unroll
                 for (int u = 0; u < U8; u++)
-                    if (j0 + NH * (2 * U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
+                    if (VR_HELPER_PREFETCH && j0 + NH * (2 * U8 + u) < tot) prefetch_l2(sp.pos4 + nxt[u]);
             }
         }
         VR_MARK(10);
@@ -489,7 +498,7 @@ __global__ void __launch_bounds__(kRowCtaThreads, 4) warp_rows_kernel(RunCtx c, 
         uint32_t v = lds_u32(ai), cand = lds_u32(ax + 4);
         for (;;) {
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < VR_TRIP_UNROLL; u++) {
                 const bool live = p < n;
                 // off the critical path (known before the probe v arrives): the slot a collision moves
                 // to, the slot the next id hashes to, and the part of the round-end test that does not
