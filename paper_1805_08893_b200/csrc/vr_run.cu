@@ -1458,7 +1458,10 @@ __global__ void __launch_bounds__(1024) scan_down_kernel(RunCtx c) {
 // K3: one warp per segment.
 // ---------------------------------------------------------------------------------
 constexpr int kShadeThreads = 256;
-constexpr int kShadeUnroll = 4;
+#ifndef VR_SHADE_UNROLL
+#define VR_SHADE_UNROLL 4
+#endif
+constexpr int kShadeUnroll = VR_SHADE_UNROLL;
 
 // Streams `cnt` staged unique ids src[0..cnt) to outputs dst0.. with `width` cooperating lanes
 // (l = lane within the group): coalesced id load, 16-byte gather, transform, coalesced stores.
